@@ -1,0 +1,322 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 online IS-NMF engine (BASELINE.json metric).
+
+Metric: online IS-NMF frames/s at F=513, K=50, beta=4096, I=10 (config 3,
+"twelve hours" shape: N=2.7M frames, rho=0.99^(beta/1000) per mini-batch,
+1 pass = one step) on one B200, plus % of the FP32 roofline.
+
+  value  — frames/s with V resident in HBM (one step = one pass over N frames
+           through isnmf_online_run with a device pointer)
+  e2e    — the same pass through the same C-ABI call with V in pinned HOST
+           memory: the engine streams 64-mini-batch chunks H2D on a copy stream,
+           double-buffered; W/A/B and the trace are read back every step
+  roofline — K1 (solve_kernel) achieved FP32 TFLOP/s = algorithmic flops per
+           launch (6*F*K*(I+1) per frame x frames per launch) / mean launch time
+           from CUDA events recorded around every K1 launch on the engine's
+           compute stream during the timed region
+  cpu_baseline — the CPU fp64 oracle (restatement of the reference; the
+           reference itself cannot be compiled: no Eigen) on a bounded prefix.
+
+`--impl reference` times that CPU implementation of the path with all host
+threads on a bounded sample per step (rank 0 only under torchrun).
+Multi-GPU: replicas only (north_star: one GPU); each rank runs its own pass,
+value = sum of frames over ranks / max time over ranks (weak scaling).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+
+from tools.synth import CONFIGS  # noqa: E402
+
+MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FP32_PEAK_FALLBACK = 72.4  # TFLOP/s, tools/probe measured on this pool (profiles/r01_probe.txt)
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=3)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="engine", choices=["engine", "reference"])
+    p.add_argument("--config", default="c3")
+    p.add_argument("--frames", type=int, default=0, help="override N (debug)")
+    p.add_argument("--cpu-sample-batches", type=int, default=4)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    return p.parse_args()
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu):
+        self.gpu, self.rows, self.proc = gpu, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": float(self.rows[0][1]),
+                "samples": len(self.rows), "reasons": reasons}
+
+
+def dist_init():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+    return rank, world
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def allmax(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def roofline_peak():
+    return FP32_PEAK_FALLBACK
+
+
+def cpu_baseline(cfg, v_host_cols, w0, a0, threads, batches):
+    """Oracle online pass over a bounded prefix (`batches` mini-batches)."""
+    import oracle as O
+    F, K, beta, iters = cfg["F"], cfg["K"], cfg["beta"], cfg["iters"]
+    n = beta * batches
+    sample = np.asfortranarray(v_host_cols[:, :n])
+    t0 = time.perf_counter()
+    O.baseline_online(sample, w0, a0, a0, beta, iters, cfg["rho"], threads=threads)
+    dt = time.perf_counter() - t0
+    return n / dt, dt, n
+
+
+def host_info():
+    cpu = "unknown"
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                cpu = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return cpu, os.cpu_count()
+
+
+def run_reference(args, rank, world):
+    cfg = dict(CONFIGS[args.config])
+    if rank != 0:
+        return
+    from tools.synth import spectrogram_np, w_init
+    F, K, beta = cfg["F"], cfg["K"], cfg["beta"]
+    threads = os.cpu_count() or 1
+    batches = max(threads, args.cpu_sample_batches)
+    v = spectrogram_np(F, K, beta * batches, seed=1234)
+    w0 = w_init(F, K, 4321)
+    a0 = np.full((F, K), 1e-3)
+    for _ in range(args.warmup if args.warmup < 1 else 1):
+        cpu_baseline(cfg, v, w0, a0, threads, 1)
+    rates, times = [], []
+    for _ in range(args.steps):
+        r, dt, n = cpu_baseline(cfg, v, w0, a0, threads, batches)
+        rates.append(r)
+        times.append(dt)
+    val = float(np.mean(rates))
+    cpu, ncpu = host_info()
+    line = {"impl": "reference", "metric": "online IS-NMF frames/sec (F=513,K=50,beta=4096)", "value": val,
+            "unit": "frames/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * float(np.mean(times)), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config}: F={F}, K={K}, beta={beta}, I={cfg['iters']}, "
+                                   f"rho={cfg['rho']:.6f}; CPU sample {beta * batches} frames per step",
+                       "parallelism": f"{threads} host threads"},
+            "cpu_baseline": {"value": val, "unit": "frames/s", "cores": threads, "kind": "port",
+                             "sample": f"{batches} mini-batches x {beta} frames of the {args.config} shape "
+                                       f"per step; fp64 oracle restatement (reference unbuildable: no Eigen); "
+                                       f"{cpu}"},
+            "e2e": {"value": val, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_engine(args, rank, world):
+    import torch
+
+    import paper_1106_4198_b200 as E
+    from tools.synth import spectrogram_torch, w_init
+    ndev = torch.cuda.device_count()
+    dev = int(os.environ.get("LOCAL_RANK", rank)) % max(ndev, 1)
+    torch.cuda.set_device(dev)
+    cfg = dict(CONFIGS[args.config])
+    F, K, beta, iters = cfg["F"], cfg["K"], cfg["beta"], cfg["iters"]
+    N = args.frames or cfg["N"]
+    rho = cfg["rho"]
+    flops_per_frame = 6.0 * F * K * (iters + 1)
+
+    # synthetic V (device) + pinned host copy for e2e
+    vd = spectrogram_torch(F, K, N, seed=1000 + rank, shape=cfg["shape"], device="cuda")
+    torch.cuda.synchronize()
+    w0 = w_init(F, K, 77 + rank)
+    a0 = np.full((F, K), 1e-3)
+
+    eng = E.Online(F, K, beta, iters, restart="warm", n_store=N)
+    eng.set_dictionary(w0, a0, a0)
+    eng.set_counters(0, 0, rho)
+    eng.fill_warm_h(1.0)
+    L = E.lib()
+
+    def one_pass(frames):
+        eng.enqueue(frames, N, frames.stride(0))
+
+    # warm-up
+    for _ in range(args.warmup):
+        one_pass(vd)
+    eng.synchronize()
+
+    # timed region: K passes, V resident in HBM
+    launches0 = eng.launch_count()
+    prof = E.Profile(eng)
+    prof.start()
+    barrier(world)
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev) as clk:
+        ev0.record()
+        t_wall = time.perf_counter()
+        for _ in range(args.steps):
+            one_pass(vd)
+        eng.synchronize()
+        ev1.record()
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t_wall
+    barrier(world)
+    # the engine runs on its own stream; eng.synchronize() bounds it, so the
+    # device interval is taken from the engine's own event span (max with torch's)
+    kstats = prof.stop()
+    ms_total = max(ev0.elapsed_time(ev1), kstats["span_ms"])
+    launches = eng.launch_count() - launches0
+    ms_total = allmax(ms_total, world)
+    value = world * N * args.steps / (ms_total / 1e3)
+    st = eng.state()
+
+    # roofline of K1
+    k1_ms = kstats["solve_ms"] / max(1, kstats["solve_launches"])
+    frames_per_launch = kstats["solve_frames"] / max(1, kstats["solve_launches"])
+    achieved = flops_per_frame * frames_per_launch / (k1_ms / 1e3) / 1e12
+    peak = roofline_peak()
+
+    # e2e: same call with host (pinned) frames, W read back every step
+    e2e = None
+    if not args.no_e2e:
+        vh = torch.empty_like(vd, device="cpu").pin_memory()
+        vh.copy_(vd)
+        del vd
+        torch.cuda.empty_cache()
+        one_pass(vh)
+        eng.synchronize()
+        wbuf = np.empty((F, K), order="F")
+        barrier(world)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            one_pass(vh)
+            eng.synchronize()
+            E.lib().isnmf_online_get_dictionary(eng._h, E._p(wbuf), None, None)
+        e2e_s = allmax(time.perf_counter() - t0, world)
+        e2e = {"value": world * N * args.steps / e2e_s, "unit": "frames/s",
+               "h2d_bytes_per_step": int(N * F * 4), "d2h_bytes_per_step": int(F * K * 8),
+               "h2d_gbs": N * F * 4 * args.steps / e2e_s / 1e9}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        from tools.synth import spectrogram_np
+        batches = args.cpu_sample_batches
+        vs = spectrogram_np(F, K, beta * batches, seed=55)
+        r, dt, n = cpu_baseline(cfg, vs, w0, a0, 1, batches)
+        cpu_name, ncpu = host_info()
+        cpu = {"value": r, "unit": "frames/s", "cores": 1, "kind": "port",
+               "sample": f"first {batches} mini-batches ({n} frames, {dt:.1f} s) of the {args.config} shape, "
+                         f"fp64 oracle restatement of the reference path on 1 core of {cpu_name} "
+                         f"({ncpu} cores); the reference itself cannot be compiled (no Eigen)"}
+
+    if rank == 0:
+        line = {"metric": "online IS-NMF frames/sec (F=513,K=50,beta=4096)", "value": value, "unit": "frames/s",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": ms_total / args.steps, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": f"{args.config}: F={F}, K={K}, beta={beta}, I={iters}, N={N}, "
+                                       f"rho={rho:.6f}, warm store h0=1, 1 pass per step",
+                           "global_batch": beta, "parallelism": "replicas" if world > 1 else "single",
+                           "l2": "inputs larger than L2 (V = %.2f GB fp32)" % (N * F * 4 / 1e9)},
+                "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                             "frac": achieved / peak, "traffic": None,
+                             "kernel": "solve_kernel<13,7>", "ms_per_launch": k1_ms,
+                             "flops_per_launch": flops_per_frame * frames_per_launch,
+                             "k1_share_of_step": kstats["solve_ms"] / ms_total,
+                             "peak_source": "FP32 FMA peak measured by tools/probe on this pool (72.4 TFLOP/s); "
+                                            "nominal 148 SM x 128 x 2 x 1.965 GHz = 74.4"},
+                "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches,
+                "clocks": clk.summary(), "wall_s": wall,
+                "final": {"t": st["t"], "commits": st["commits"], "last_minibatch_obj": st["last_minibatch_obj"]}}
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank, world = dist_init()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_engine(args, rank, world)
+
+
+if __name__ == "__main__":
+    main()

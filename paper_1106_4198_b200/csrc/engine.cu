@@ -1,0 +1,1390 @@
+// Host side of the B200 IS-NMF engine: device contexts, launch orchestration,
+// H2D streaming and the extern "C" boundary declared in include/isnmf_b200.h.
+//
+// The online path follows online_resume / online_step / dictionary_commit
+// (reference proj/include/isnmf/online.hpp:318-407): frames are processed in
+// blocks that never cross a mini-batch boundary; a block is one K1 launch
+// (all frames of the block solved and their statistics formed in parallel —
+// W is frozen inside a mini-batch, so this equals the sequential per-sample
+// loop up to fp rounding), one K2 launch (fixed-order reduction into pending,
+// plus the elementwise commit on the beta-th sample) and, on a commit, one K3
+// launch (column renormalisation, trace point, eta stop rule).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <unordered_set>
+#include <vector>
+
+#include "../../include/isnmf_b200.h"
+#include "kernels.cuh"
+
+using namespace isnmf_dev;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CU(x)                                                                                    \
+  do {                                                                                           \
+    cudaError_t e_ = (x);                                                                        \
+    if (e_ != cudaSuccess) return fail(ISNMF_E_CUDA, "%s: %s (%s:%d)", #x, cudaGetErrorString(e_), \
+                                       __FILE__, __LINE__);                                      \
+  } while (0)
+
+#define TRY(x)             \
+  do {                     \
+    int rc_ = (x);         \
+    if (rc_) return rc_;   \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// Kernel family: solve_kernel<TK, TN> handles K <= 4*TK atoms and 4*TN frames
+// per CTA.  The variant is picked per context so that one mini-batch fills the
+// 148 SMs in a single wave.
+// ---------------------------------------------------------------------------
+using SolveFn = void (*)(const SolveArgs);
+struct Variant {
+  int TK, TN;
+  SolveFn fn;
+  size_t (*smem)(int, int);
+  size_t static_smem;
+  bool configured;
+};
+
+#define VAR(tk, tn) {tk, tn, solve_kernel<tk, tn>, &SolveShape<tk, tn>::smem_bytes, 0, false}
+Variant g_variants[] = {
+    VAR(1, 1), VAR(1, 2), VAR(1, 4), VAR(1, 7), VAR(1, 8),       //
+    VAR(2, 1), VAR(2, 2), VAR(2, 4), VAR(2, 7), VAR(2, 8),       //
+    VAR(3, 1), VAR(3, 2), VAR(3, 4), VAR(3, 7), VAR(3, 8),       //
+    VAR(5, 1), VAR(5, 2), VAR(5, 4), VAR(5, 7), VAR(5, 8),       //
+    VAR(8, 1), VAR(8, 2), VAR(8, 4), VAR(8, 7), VAR(8, 8),       //
+    VAR(13, 1), VAR(13, 2), VAR(13, 4), VAR(13, 7), VAR(13, 8),  //
+    VAR(16, 1), VAR(16, 2), VAR(16, 4), VAR(16, 7),              //
+};
+#undef VAR
+constexpr int kNumVariants = sizeof(g_variants) / sizeof(g_variants[0]);
+
+int device_sms() {
+  static int sms = -1;
+  if (sms < 0) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) !=
+                                                  cudaSuccess)
+      sms = 148;
+  }
+  return sms;
+}
+
+int smem_optin() {
+  static int v = -1;
+  if (v < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) v = 232448;
+  }
+  return v;
+}
+
+int ws_for(int KP) { return ((KP / 4) % 2 == 1) ? KP : KP + 4; }
+
+// Picks the variant for (F, K, frames per mini-batch).
+int pick_variant(int64_t F, int64_t K, int64_t frames, Variant** out, int* WS, size_t* smem) {
+  const int tk_need = int((K + 3) / 4);
+  const int64_t per_cta = (frames + device_sms() - 1) / device_sms();
+  const int tn_need = int(std::min<int64_t>(8, std::max<int64_t>(1, (per_cta + 3) / 4)));
+  Variant* best = nullptr;
+  for (auto& v : g_variants) {
+    if (v.TK < tk_need || v.TN < tn_need) continue;
+    if (!best || v.TK < best->TK || (v.TK == best->TK && v.TN < best->TN)) best = &v;
+  }
+  if (!best) {  // TN capped by the table: take the largest TN for the smallest TK
+    for (auto& v : g_variants) {
+      if (v.TK < tk_need) continue;
+      if (!best || v.TK < best->TK || (v.TK == best->TK && v.TN > best->TN)) best = &v;
+    }
+  }
+  if (!best) return fail(ISNMF_E_UNSUPPORTED, "K=%lld exceeds the built kernel family (K <= 64)", (long long)K);
+  const int w = ws_for(4 * best->TK);
+  if (!best->configured) {
+    cudaFuncAttributes at;
+    CU(cudaFuncGetAttributes(&at, best->fn));
+    best->static_smem = at.sharedSizeBytes;
+    CU(cudaFuncSetAttribute(best->fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            smem_optin() - int(best->static_smem)));
+    best->configured = true;
+  }
+  const size_t sm = best->smem(int(F), w);
+  if (sm + best->static_smem > size_t(smem_optin()))
+    return fail(ISNMF_E_UNSUPPORTED, "F=%lld, K=%lld: dictionary (%zu B) does not fit shared memory", (long long)F,
+                (long long)K, sm);
+  *out = best;
+  *WS = w;
+  *smem = sm;
+  return 0;
+}
+
+template <class T>
+int dalloc(T** p, size_t n) {
+  *p = nullptr;
+  if (n == 0) n = 1;
+  CU(cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(T)));
+  return 0;
+}
+
+void dfree(void* p) {
+  if (p) cudaFree(p);
+}
+
+// col-major F x K (host, fp64) <-> row-major [F][K]
+void to_rowmajor(const double* cm, int64_t F, int64_t K, double* rm) {
+  for (int64_t k = 0; k < K; ++k)
+    for (int64_t f = 0; f < F; ++f) rm[f * K + k] = cm[k * F + f];
+}
+void to_colmajor(const double* rm, int64_t F, int64_t K, double* cm) {
+  for (int64_t k = 0; k < K; ++k)
+    for (int64_t f = 0; f < F; ++f) cm[k * F + f] = rm[f * K + k];
+}
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+__global__ void fill_f32(float* p, int64_t n, float v) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    p[i] = v;
+}
+__global__ void fill_u32(uint32_t* p, int64_t n, uint32_t v) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    p[i] = v;
+}
+__global__ void fill_f64(double* p, int64_t n, double v) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    p[i] = v;
+}
+// U[col] <- current value (U * P[c]/P[T]), T <- c_new.
+__global__ void warm_rebase(float* U, uint32_t* T, const double* P, int64_t n, int K, uint32_t c_old,
+                            uint32_t c_new) {
+  for (int64_t col = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; col < n; col += int64_t(gridDim.x) * blockDim.x) {
+    const uint32_t tag = T[col];
+    for (int k = 0; k < K; ++k)
+      U[col * K + k] = float(double(U[col * K + k]) * (P[size_t(c_old) * K + k] / P[size_t(tag) * K + k]));
+    T[col] = c_new;
+  }
+}
+__global__ void warm_read(const float* U, const uint32_t* T, const double* P, int64_t n, int K, uint32_t c,
+                          double* out) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n * K; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t col = i / K;
+    const int k = int(i - col * K);
+    out[i] = double(U[i]) * (P[size_t(c) * K + k] / P[size_t(T[col]) * K + k]);
+  }
+}
+__global__ void mark_origin(DevState* st) { st->origin_ns = globaltimer_ns(); }
+
+int status_to_code(unsigned int s, const char* where, unsigned long long t) {
+  if (s & ST_NONPOS_INIT) return fail(ISNMF_E_NON_POSITIVE_INIT, "%s: h0 must be positive (t = %llu)", where, t);
+  if (s & ST_INCONSISTENT) return fail(ISNMF_E_INCONSISTENT_STATS, "update_w: a > 0 with b = 0 (t = %llu)", t);
+  if (s & ST_NONFINITE_W)
+    return fail(ISNMF_E_NUMERICAL_FAILURE, "%s: non-finite dictionary update at t = %llu", where, t);
+  if (s & ST_ZERO_COLUMN) return fail(ISNMF_E_ZERO_COLUMN, "rescale_dictionary: dead atom (t = %llu)", t);
+  if (s & ST_DIVERGED) return fail(ISNMF_E_DIVERGED_OBJECTIVE, "%s: objective increased", where);
+  return fail(ISNMF_E_CUDA, "%s: unknown device status %u", where, s);
+}
+
+}  // namespace
+
+// ===========================================================================
+// Online context
+// ===========================================================================
+struct isnmf_online {
+  isnmf_online_config cfg{};
+  int F = 0, K = 0, beta = 0, iters = 0, restart = 0;
+  double eps = 0.0;
+  Variant* var = nullptr;
+  int WS = 0, KP = 0, NT = 0;
+  size_t smem = 0;
+  cudaStream_t cs = nullptr, xs = nullptr;
+  DevState* st = nullptr;
+  double *W64 = nullptr, *A = nullptr, *B = nullptr, *pa = nullptr, *pb = nullptr, *Wtmp = nullptr;
+  double* colpart = nullptr;
+  double* P = nullptr;
+  int64_t Pcap = 0;
+  float* W32 = nullptr;
+  float* stats = nullptr;
+  double* divpart = nullptr;
+  int maxblk = 0;
+  float* U = nullptr;
+  uint32_t* T = nullptr;
+  int64_t nstore = 0;
+  double* u01 = nullptr;
+  float* Hlast = nullptr;
+  unsigned long long* tr_t = nullptr;
+  double* tr_obj = nullptr;
+  unsigned long long* tr_ns = nullptr;
+  int64_t tr_cap = 0;
+  float* vbuf[2] = {nullptr, nullptr};
+  uint64_t* ibuf[2] = {nullptr, nullptr};
+  int64_t chunk = 0;
+  cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
+  uint64_t t_host = 0, commits_host = 0, trace_base = 0;
+  double rho = 1.0;
+  double eta = 0.0;
+  int64_t launches = 0;
+  // profiling (isnmf_online_profile_begin/end)
+  bool prof = false;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  int64_t prof_frames = 0;
+  cudaEvent_t ev_span[2] = {nullptr, nullptr};
+};
+
+namespace {
+
+int online_free(isnmf_online* c) {
+  if (!c) return 0;
+  if (c->cs) cudaStreamSynchronize(c->cs);
+  if (c->xs) cudaStreamSynchronize(c->xs);
+  void* ptrs[] = {c->st, c->W64, c->A, c->B, c->pa, c->pb, c->Wtmp, c->colpart, c->P, c->W32, c->stats,
+                  c->divpart, c->U, c->T, c->u01, c->Hlast, c->tr_t, c->tr_obj, c->tr_ns, c->vbuf[0],
+                  c->vbuf[1], c->ibuf[0], c->ibuf[1]};
+  for (void* p : ptrs) dfree(p);
+  for (int i = 0; i < 2; ++i) {
+    if (c->ev_copied[i]) cudaEventDestroy(c->ev_copied[i]);
+    if (c->ev_free[i]) cudaEventDestroy(c->ev_free[i]);
+    if (c->ev_span[i]) cudaEventDestroy(c->ev_span[i]);
+  }
+  for (auto e : c->ev_pool) cudaEventDestroy(e);
+  if (c->cs) cudaStreamDestroy(c->cs);
+  if (c->xs) cudaStreamDestroy(c->xs);
+  delete c;
+  return 0;
+}
+
+int read_state(isnmf_online* c, DevState* h) {
+  CU(cudaStreamSynchronize(c->cs));
+  CU(cudaMemcpy(h, c->st, sizeof(DevState), cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+// Grows the P table (prefix products of column scales) to hold `rows` rows.
+int ensure_P(isnmf_online* c, int64_t rows) {
+  if (rows <= c->Pcap) return 0;
+  int64_t cap = std::max<int64_t>(rows, 2 * c->Pcap + 64);
+  double* np = nullptr;
+  TRY(dalloc(&np, size_t(cap) * c->K));
+  CU(cudaStreamSynchronize(c->cs));
+  if (c->P) CU(cudaMemcpy(np, c->P, size_t(c->Pcap) * c->K * sizeof(double), cudaMemcpyDeviceToDevice));
+  dfree(c->P);
+  c->P = np;
+  c->Pcap = cap;
+  return 0;
+}
+
+int ensure_trace(isnmf_online* c, int64_t n) {
+  if (n <= c->tr_cap) return 0;
+  int64_t cap = std::max<int64_t>(n, 2 * c->tr_cap + 64);
+  unsigned long long *t = nullptr, *ns = nullptr;
+  double* o = nullptr;
+  TRY(dalloc(&t, cap));
+  TRY(dalloc(&ns, cap));
+  TRY(dalloc(&o, cap));
+  CU(cudaStreamSynchronize(c->cs));
+  if (c->tr_cap) {
+    CU(cudaMemcpy(t, c->tr_t, c->tr_cap * sizeof(*t), cudaMemcpyDeviceToDevice));
+    CU(cudaMemcpy(ns, c->tr_ns, c->tr_cap * sizeof(*ns), cudaMemcpyDeviceToDevice));
+    CU(cudaMemcpy(o, c->tr_obj, c->tr_cap * sizeof(*o), cudaMemcpyDeviceToDevice));
+  }
+  dfree(c->tr_t);
+  dfree(c->tr_ns);
+  dfree(c->tr_obj);
+  c->tr_t = t;
+  c->tr_ns = ns;
+  c->tr_obj = o;
+  c->tr_cap = cap;
+  return 0;
+}
+
+// One block of nb frames inside a single mini-batch: K0? -> K1 -> K2 (-> K3).
+int launch_block(isnmf_online* c, const float* dv, int64_t ldv, int nb, const uint64_t* widx_dev) {
+  const int nblk = (nb + c->NT - 1) / c->NT;
+  if (c->restart == ISNMF_RESTART_FRESH) {
+    fresh_kernel<<<(nb + 127) / 128, 128, 0, c->cs>>>(c->cfg.seed, c->t_host, nb, c->K, c->u01);
+    c->launches++;
+  }
+  SolveArgs a{};
+  a.W32 = c->W32;
+  a.F = c->F;
+  a.K = c->K;
+  a.WS = c->WS;
+  a.V = dv;
+  a.ldv = ldv;
+  a.vsel = nullptr;
+  a.v0 = 0;
+  a.nframes = nb;
+  a.iters = c->iters;
+  a.eps = float(c->eps);
+  a.epsd = c->eps;
+  a.h0_mode = c->restart == ISNMF_RESTART_WARM ? 1 : 2;
+  a.U = c->U;
+  a.T = c->T;
+  a.P = c->P;
+  a.c_now = uint32_t(c->commits_host);
+  a.widx = widx_dev;
+  a.wbase = c->nstore ? int64_t(c->t_host % uint64_t(c->nstore)) : 0;
+  a.wmod = c->nstore ? c->nstore : 1;
+  a.u01 = c->u01;
+  a.kst = c->st;
+  a.Hout = c->Hlast + size_t(c->t_host % uint64_t(c->beta)) * c->K;
+  a.write_store = c->restart == ISNMF_RESTART_WARM;
+  a.check_h0 = 1;
+  a.do_stats = 1;
+  a.div_first = 0;
+  a.stats = c->stats;
+  a.divpart = c->divpart;
+  a.status = &c->st->status;
+  a.halt = &c->st->halt;
+  if (c->prof) {
+    while (c->ev_pool.size() < c->ev_used + 2) {
+      cudaEvent_t e;
+      CU(cudaEventCreate(&e));
+      c->ev_pool.push_back(e);
+    }
+    CU(cudaEventRecord(c->ev_pool[c->ev_used], c->cs));
+  }
+  c->var->fn<<<nblk, kThreads, c->smem, c->cs>>>(a);
+  if (c->prof) {
+    CU(cudaEventRecord(c->ev_pool[c->ev_used + 1], c->cs));
+    c->ev_used += 2;
+    c->prof_frames += nb;
+  }
+  const bool commit = (c->t_host + uint64_t(nb)) % uint64_t(c->beta) == 0;
+  ReduceArgs r{};
+  r.stats = c->stats;
+  r.divpart = c->divpart;
+  r.nblk = nblk;
+  r.F = c->F;
+  r.K = c->K;
+  r.KP = c->KP;
+  r.nframes = nb;
+  r.W64 = c->W64;
+  r.pa = c->pa;
+  r.pb = c->pb;
+  r.A = c->A;
+  r.B = c->B;
+  r.Wtmp = c->Wtmp;
+  r.do_commit = commit;
+  r.rho = c->rho;
+  r.st = c->st;
+  r.halt = &c->st->halt;
+  reduce_kernel<<<(c->F * c->K + 255) / 256, 256, 0, c->cs>>>(r);
+  c->launches += 2;
+  if (commit) {
+    CommitArgs m{};
+    m.F = c->F;
+    m.K = c->K;
+    m.WS = c->WS;
+    m.Wtmp = c->Wtmp;
+    m.W64 = c->W64;
+    m.A = c->A;
+    m.B = c->B;
+    m.W32 = c->W32;
+    m.P = c->P;
+    m.colpart = c->colpart;
+    m.st = c->st;
+    m.halt = &c->st->halt;
+    m.eta = c->eta;
+    m.tr_t = c->tr_t;
+    m.tr_obj = c->tr_obj;
+    m.tr_ns = c->tr_ns;
+    m.tr_cap = c->tr_cap;
+    m.batch_mode = 0;
+    commit_kernel<<<c->K, 256, 0, c->cs>>>(m);
+    c->launches++;
+    c->commits_host++;
+  }
+  c->t_host += uint64_t(nb);
+  CU(cudaGetLastError());
+  return 0;
+}
+
+// Frames [0, n) of a device-resident span, split at mini-batch boundaries and,
+// in warm mode, wherever a store column repeats inside a mini-batch (the
+// reference's sequential loop would see the first visit's update).
+int run_span(isnmf_online* c, const float* dv, int64_t ldv, int64_t n, const uint64_t* idx_host,
+             const uint64_t* idx_dev) {
+  int64_t pos = 0;
+  std::unordered_set<uint64_t> seen;
+  while (pos < n) {
+    const int64_t room = int64_t(uint64_t(c->beta) - c->t_host % uint64_t(c->beta));
+    int64_t nb = std::min<int64_t>(room, n - pos);
+    if (c->restart == ISNMF_RESTART_WARM && !idx_host) nb = std::min<int64_t>(nb, c->nstore);
+    if (c->restart == ISNMF_RESTART_WARM && idx_host) {
+      seen.clear();
+      for (int64_t j = 0; j < nb; ++j)
+        if (!seen.insert(idx_host[pos + j]).second) {
+          nb = j;
+          break;
+        }
+    }
+    TRY(launch_block(c, dv + pos * ldv, ldv, int(nb), idx_dev ? idx_dev + pos : nullptr));
+    pos += nb;
+  }
+  return 0;
+}
+
+int online_enqueue(isnmf_online* c, const float* frames, int64_t ldv, int64_t n, const uint64_t* index,
+                   uint64_t budget, double eta) {
+  if (n < 0) return fail(ISNMF_E_INVALID_ARG, "online_run: n < 0");
+  if (n > 0 && !frames) return fail(ISNMF_E_INVALID_ARG, "online_run: frames is NULL");
+  if (ldv < c->F) return fail(ISNMF_E_INVALID_ARG, "online_run: ldv < F");
+  c->eta = eta;
+  const uint64_t room = c->t_host >= budget ? 0 : budget - c->t_host;
+  const int64_t n_eff = uint64_t(n) <= room ? n : int64_t(room);
+  if (n_eff == 0) return 0;
+  if (c->restart == ISNMF_RESTART_WARM && index) {
+    for (int64_t j = 0; j < n_eff; ++j)
+      if (index[j] >= uint64_t(c->nstore))
+        return fail(ISNMF_E_SHAPE_MISMATCH, "online_step: sample index outside warm activation store");
+  }
+  const int64_t commits_max = int64_t(c->commits_host) + n_eff / c->beta + 2;
+  TRY(ensure_P(c, commits_max + 1));
+  TRY(ensure_trace(c, commits_max - int64_t(c->trace_base) + 1));
+
+  if (is_device_ptr(frames)) {
+    uint64_t* idx_dev = nullptr;
+    if (index) {
+      TRY(dalloc(&idx_dev, n_eff));
+      CU(cudaMemcpyAsync(idx_dev, index, n_eff * sizeof(uint64_t), cudaMemcpyHostToDevice, c->cs));
+    }
+    int rc = run_span(c, frames, ldv, n_eff, index, idx_dev);
+    if (idx_dev) {
+      cudaStreamSynchronize(c->cs);
+      dfree(idx_dev);
+    }
+    return rc;
+  }
+  // host frames: chunked H2D on the copy stream, double-buffered
+  if (!c->vbuf[0]) {
+    for (int i = 0; i < 2; ++i) {
+      TRY(dalloc(&c->vbuf[i], size_t(c->chunk) * c->F));
+      TRY(dalloc(&c->ibuf[i], size_t(c->chunk)));
+      CU(cudaEventCreateWithFlags(&c->ev_copied[i], cudaEventDisableTiming));
+      CU(cudaEventCreateWithFlags(&c->ev_free[i], cudaEventDisableTiming));
+      CU(cudaEventRecord(c->ev_free[i], c->cs));
+    }
+  }
+  int64_t pos = 0;
+  int buf = 0;
+  while (pos < n_eff) {
+    const int64_t cf = std::min<int64_t>(c->chunk, n_eff - pos);
+    CU(cudaStreamWaitEvent(c->xs, c->ev_free[buf], 0));
+    CU(cudaMemcpy2DAsync(c->vbuf[buf], size_t(c->F) * sizeof(float), frames + pos * ldv,
+                         size_t(ldv) * sizeof(float), size_t(c->F) * sizeof(float), size_t(cf),
+                         cudaMemcpyHostToDevice, c->xs));
+    if (index)
+      CU(cudaMemcpyAsync(c->ibuf[buf], index + pos, size_t(cf) * sizeof(uint64_t), cudaMemcpyHostToDevice, c->xs));
+    CU(cudaEventRecord(c->ev_copied[buf], c->xs));
+    CU(cudaStreamWaitEvent(c->cs, c->ev_copied[buf], 0));
+    TRY(run_span(c, c->vbuf[buf], c->F, cf, index ? index + pos : nullptr, index ? c->ibuf[buf] : nullptr));
+    CU(cudaEventRecord(c->ev_free[buf], c->cs));
+    pos += cf;
+    buf ^= 1;
+  }
+  return 0;
+}
+
+int online_finish(isnmf_online* c, int32_t* stopped) {
+  DevState h;
+  TRY(read_state(c, &h));
+  c->t_host = h.t;
+  c->commits_host = h.commits;
+  if (stopped) *stopped = int32_t(h.halt != 0);
+  if (h.status) return status_to_code(h.status, "online", h.t);
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* isnmf_last_error(void) { return g_err.c_str(); }
+
+int isnmf_device_info(char* buf, int64_t cap) {
+  int dev = 0;
+  cudaDeviceProp p;
+  CU(cudaGetDevice(&dev));
+  CU(cudaGetDeviceProperties(&p, dev));
+  std::string variants;
+  for (int i = 0; i < kNumVariants; ++i)
+    variants += (i ? "," : "") + std::to_string(g_variants[i].TK * 4) + "x" + std::to_string(g_variants[i].TN * 4);
+  const int n = snprintf(buf, size_t(cap),
+                         "{\"device\":\"%s\",\"sm\":\"%d.%d\",\"sms\":%d,\"smem_optin\":%zu,\"arch\":\"sm_100a\","
+                         "\"solve_variants_KPxNT\":\"%s\"}",
+                         p.name, p.major, p.minor, p.multiProcessorCount, p.sharedMemPerBlockOptin, variants.c_str());
+  return n < cap ? 0 : fail(ISNMF_E_INVALID_ARG, "device_info: buffer too small");
+}
+
+int isnmf_online_create(isnmf_online** out, const isnmf_online_config* cfg) {
+  if (!out || !cfg) return fail(ISNMF_E_INVALID_ARG, "online_create: NULL argument");
+  *out = nullptr;
+  if (cfg->F < 1 || cfg->K < 1) return fail(ISNMF_E_SHAPE_MISMATCH, "online_create: empty dictionary");
+  if (cfg->beta < 1) return fail(ISNMF_E_NEGATIVE_INPUT, "config: beta must be >= 1");
+  if (cfg->inner_iters < 1) return fail(ISNMF_E_NEGATIVE_INPUT, "online_create: inner_iters must be >= 1");
+  if (!(cfg->epsilon > 0.0)) return fail(ISNMF_E_NEGATIVE_INPUT, "config: epsilon must be > 0");
+  if (cfg->restart != ISNMF_RESTART_WARM && cfg->restart != ISNMF_RESTART_FRESH)
+    return fail(ISNMF_E_INVALID_ARG, "online_create: bad restart mode");
+  if (cfg->restart == ISNMF_RESTART_WARM && cfg->n_store < 1)
+    return fail(ISNMF_E_EMPTY_DATASET, "online: warm restarts need an in-memory dataset");
+  auto* c = new isnmf_online;
+  c->cfg = *cfg;
+  c->F = int(cfg->F);
+  c->K = int(cfg->K);
+  c->beta = cfg->beta;
+  c->iters = cfg->inner_iters;
+  c->restart = cfg->restart;
+  c->eps = cfg->epsilon;
+  c->nstore = cfg->restart == ISNMF_RESTART_WARM ? cfg->n_store : 0;
+  c->chunk = cfg->max_chunk > 0 ? cfg->max_chunk : int64_t(64) * cfg->beta;
+  int rc = pick_variant(c->F, c->K, c->beta, &c->var, &c->WS, &c->smem);
+  auto bail = [&](int code) {
+    std::string keep = g_err;
+    online_free(c);
+    g_err = keep;
+    return code;
+  };
+  if (rc) return bail(rc);
+  c->KP = 4 * c->var->TK;
+  c->NT = 4 * c->var->TN;
+  c->maxblk = (c->beta + c->NT - 1) / c->NT;
+  const size_t FK = size_t(c->F) * c->K;
+  if (cudaStreamCreateWithFlags(&c->cs, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->xs, cudaStreamNonBlocking) != cudaSuccess)
+    return bail(fail(ISNMF_E_CUDA, "online_create: stream creation failed (%s)",
+                     cudaGetErrorString(cudaGetLastError())));
+  if ((rc = dalloc(&c->st, 1)) || (rc = dalloc(&c->W64, FK)) || (rc = dalloc(&c->A, FK)) ||
+      (rc = dalloc(&c->B, FK)) || (rc = dalloc(&c->pa, FK)) || (rc = dalloc(&c->pb, FK)) ||
+      (rc = dalloc(&c->Wtmp, FK)) || (rc = dalloc(&c->colpart, 2 * size_t(c->K))) ||
+      (rc = dalloc(&c->W32, size_t(c->F) * c->WS)) ||
+      (rc = dalloc(&c->stats, size_t(c->maxblk) * 2 * c->F * c->KP)) || (rc = dalloc(&c->divpart, c->maxblk)) ||
+      (rc = dalloc(&c->Hlast, size_t(c->beta) * c->K)))
+    return bail(rc);
+  if (c->restart == ISNMF_RESTART_FRESH && (rc = dalloc(&c->u01, size_t(c->beta) * c->K))) return bail(rc);
+  if (c->restart == ISNMF_RESTART_WARM &&
+      ((rc = dalloc(&c->U, size_t(c->nstore) * c->K)) || (rc = dalloc(&c->T, size_t(c->nstore)))))
+    return bail(rc);
+  if ((rc = ensure_P(c, 64)) || (rc = ensure_trace(c, 64))) return bail(rc);
+  DevState h{};
+  h.last_delta = INFINITY;
+  h.kmeanw = 1.0;
+  if (cudaMemcpy(c->st, &h, sizeof(h), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemset(c->W32, 0, size_t(c->F) * c->WS * sizeof(float)) != cudaSuccess ||
+      cudaMemset(c->pa, 0, FK * sizeof(double)) != cudaSuccess ||
+      cudaMemset(c->pb, 0, FK * sizeof(double)) != cudaSuccess ||
+      cudaMemset(c->Hlast, 0, size_t(c->beta) * c->K * sizeof(float)) != cudaSuccess)
+    return bail(fail(ISNMF_E_CUDA, "online_create: init failed (%s)", cudaGetErrorString(cudaGetLastError())));
+  fill_f64<<<64, 256, 0, c->cs>>>(c->P, c->Pcap * c->K, 1.0);
+  if (c->restart == ISNMF_RESTART_WARM) {
+    fill_f32<<<592, 256, 0, c->cs>>>(c->U, c->nstore * c->K, 1.0f);
+    fill_u32<<<592, 256, 0, c->cs>>>(c->T, c->nstore, 0u);
+  }
+  mark_origin<<<1, 1, 0, c->cs>>>(c->st);
+  if (cudaStreamSynchronize(c->cs) != cudaSuccess)
+    return bail(fail(ISNMF_E_CUDA, "online_create: %s", cudaGetErrorString(cudaGetLastError())));
+  *out = c;
+  return 0;
+}
+
+int isnmf_online_destroy(isnmf_online* c) { return online_free(c); }
+
+int isnmf_online_set_dictionary(isnmf_online* c, const double* w, const double* a, const double* b) {
+  if (!c) return fail(ISNMF_E_INVALID_ARG, "NULL context");
+  const int64_t F = c->F, K = c->K;
+  std::vector<double> rm(size_t(F * K));
+  CU(cudaStreamSynchronize(c->cs));
+  if (w) {
+    to_rowmajor(w, F, K, rm.data());
+    CU(cudaMemcpy(c->W64, rm.data(), rm.size() * sizeof(double), cudaMemcpyHostToDevice));
+    std::vector<float> w32(size_t(F) * c->WS, 0.0f);
+    double sum = 0.0;
+    for (int64_t k = 0; k < K; ++k)
+      for (int64_t f = 0; f < F; ++f) {
+        w32[f * c->WS + k] = float(w[k * F + f]);
+        sum += w[k * F + f];
+      }
+    CU(cudaMemcpy(c->W32, w32.data(), w32.size() * sizeof(float), cudaMemcpyHostToDevice));
+    const double kmeanw = double(K) * (sum / double(F * K));
+    CU(cudaMemcpy(reinterpret_cast<char*>(c->st) + offsetof(DevState, kmeanw), &kmeanw, sizeof(double),
+                  cudaMemcpyHostToDevice));
+  }
+  if (a) {
+    to_rowmajor(a, F, K, rm.data());
+    CU(cudaMemcpy(c->A, rm.data(), rm.size() * sizeof(double), cudaMemcpyHostToDevice));
+  }
+  if (b) {
+    to_rowmajor(b, F, K, rm.data());
+    CU(cudaMemcpy(c->B, rm.data(), rm.size() * sizeof(double), cudaMemcpyHostToDevice));
+  }
+  return 0;
+}
+
+int isnmf_online_get_dictionary(isnmf_online* c, double* w, double* a, double* b) {
+  if (!c) return fail(ISNMF_E_INVALID_ARG, "NULL context");
+  const int64_t F = c->F, K = c->K;
+  std::vector<double> rm(size_t(F * K));
+  CU(cudaStreamSynchronize(c->cs));
+  double* src[3] = {c->W64, c->A, c->B};
+  double* dst[3] = {w, a, b};
+  for (int i = 0; i < 3; ++i)
+    if (dst[i]) {
+      CU(cudaMemcpy(rm.data(), src[i], rm.size() * sizeof(double), cudaMemcpyDeviceToHost));
+      to_colmajor(rm.data(), F, K, dst[i]);
+    }
+  return 0;
+}
+
+int isnmf_online_set_pending(isnmf_online* c, const double* pa, const double* pb, double pending_div,
+                             uint64_t pending_count) {
+  if (!c) return fail(ISNMF_E_INVALID_ARG, "NULL context");
+  const int64_t F = c->F, K = c->K;
+  std::vector<double> rm(size_t(F * K));
+  CU(cudaStreamSynchronize(c->cs));
+  if (pa) {
+    to_rowmajor(pa, F, K, rm.data());
+    CU(cudaMemcpy(c->pa, rm.data(), rm.size() * sizeof(double), cudaMemcpyHostToDevice));
+  }
+  if (pb) {
+    to_rowmajor(pb, F, K, rm.data());
+    CU(cudaMemcpy(c->pb, rm.data(), rm.size() * sizeof(double), cudaMemcpyHostToDevice));
+  }
+  DevState h;
+  CU(cudaMemcpy(&h, c->st, sizeof(h), cudaMemcpyDeviceToHost));
+  h.pending_div = pending_div;
+  h.pending_count = pending_count;
+  CU(cudaMemcpy(c->st, &h, sizeof(h), cudaMemcpyHostToDevice));
+  return 0;
+}
+
+int isnmf_online_get_pending(isnmf_online* c, double* pa, double* pb, double* pending_div, uint64_t* pending_count) {
+  if (!c) return fail(ISNMF_E_INVALID_ARG, "NULL context");
+  const int64_t F = c->F, K = c->K;
+  std::vector<double> rm(size_t(F * K));
+  CU(cudaStreamSynchronize(c->cs));
+  if (pa) {
+    CU(cudaMemcpy(rm.data(), c->pa, rm.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    to_colmajor(rm.data(), F, K, pa);
+  }
+  if (pb) {
+    CU(cudaMemcpy(rm.data(), c->pb, rm.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    to_colmajor(rm.data(), F, K, pb);
+  }
+  DevState h;
+  CU(cudaMemcpy(&h, c->st, sizeof(h), cudaMemcpyDeviceToHost));
+  if (pending_div) *pending_div = h.pending_div;
+  if (pending_count) *pending_count = h.pending_count;
+  return 0;
+}
+
+int isnmf_online_set_counters(isnmf_online* c, uint64_t t, uint64_t commits, double rho) {
+  if (!c) return fail(ISNMF_E_INVALID_ARG, "NULL context");
+  if (!(rho >= 0.0)) return fail(ISNMF_E_NEGATIVE_INPUT, "rho must be >= 0");
+  CU(cudaStreamSynchronize(c->cs));
+  const uint64_t c_old = c->commits_host;
+  TRY(ensure_P(c, int64_t(std::max(commits, c_old)) + 2));
+  if (commits != c_old) {
+    // P[commits] <- 1 and re-tag the warm store at its current values
+    if (c->restart == ISNMF_RESTART_WARM)
+      warm_rebase<<<592, 256, 0, c->cs>>>(c->U, c->T, c->P, c->nstore, c->K, uint32_t(c_old), uint32_t(commits));
+    fill_f64<<<1, 256, 0, c->cs>>>(c->P + size_t(commits) * c->K, c->K, 1.0);
+    if (c->restart == ISNMF_RESTART_WARM) {
+      // tags now equal `commits`, whose P row is 1: values unchanged
+    }
+    CU(cudaStreamSynchronize(c->cs));
+  }
+  DevState h;
+  CU(cudaMemcpy(&h, c->st, sizeof(h), cudaMemcpyDeviceToHost));
+  h.t = t;
+  h.commits = commits;
+  h.trace_base = commits;
+  h.halt = 0;
+  CU(cudaMemcpy(c->st, &h, sizeof(h), cudaMemcpyHostToDevice));
+  c->t_host = t;
+  c->commits_host = commits;
+  c->trace_base = commits;
+  c->rho = rho;
+  return 0;
+}
+
+int isnmf_online_get_counters(isnmf_online* c, uint64_t* t, uint64_t* commits, double* rho, double* last_delta,
+                              double* last_obj) {
+  if (!c) return fail(ISNMF_E_INVALID_ARG, "NULL context");
+  DevState h;
+  TRY(read_state(c, &h));
+  if (t) *t = h.t;
+  if (commits) *commits = h.commits;
+  if (rho) *rho = c->rho;
+  if (last_delta) *last_delta = h.last_delta;
+  if (last_obj) *last_obj = h.last_obj;
+  return 0;
+}
+
+int isnmf_online_set_warm_h(isnmf_online* c, const double* warm_h) {
+  if (!c || !warm_h) return fail(ISNMF_E_INVALID_ARG, "NULL argument");
+  if (c->restart != ISNMF_RESTART_WARM) return fail(ISNMF_E_INVALID_ARG, "set_warm_h: context is not warm");
+  std::vector<float> u(size_t(c->nstore) * c->K);
+  for (size_t i = 0; i < u.size(); ++i) u[i] = float(warm_h[i]);
+  CU(cudaStreamSynchronize(c->cs));
+  CU(cudaMemcpy(c->U, u.data(), u.size() * sizeof(float), cudaMemcpyHostToDevice));
+  fill_u32<<<592, 256, 0, c->cs>>>(c->T, c->nstore, uint32_t(c->commits_host));
+  fill_f64<<<1, 256, 0, c->cs>>>(c->P + size_t(c->commits_host) * c->K, c->K, 1.0);
+  CU(cudaStreamSynchronize(c->cs));
+  return 0;
+}
+
+int isnmf_online_fill_warm_h(isnmf_online* c, double value) {
+  if (!c) return fail(ISNMF_E_INVALID_ARG, "NULL context");
+  if (c->restart != ISNMF_RESTART_WARM) return fail(ISNMF_E_INVALID_ARG, "fill_warm_h: context is not warm");
+  fill_f32<<<592, 256, 0, c->cs>>>(c->U, c->nstore * c->K, float(value));
+  fill_u32<<<592, 256, 0, c->cs>>>(c->T, c->nstore, uint32_t(c->commits_host));
+  fill_f64<<<1, 256, 0, c->cs>>>(c->P + size_t(c->commits_host) * c->K, c->K, 1.0);
+  CU(cudaStreamSynchronize(c->cs));
+  return 0;
+}
+
+int isnmf_online_get_warm_h(isnmf_online* c, double* warm_h) {
+  if (!c || !warm_h) return fail(ISNMF_E_INVALID_ARG, "NULL argument");
+  if (c->restart != ISNMF_RESTART_WARM) return fail(ISNMF_E_INVALID_ARG, "get_warm_h: context is not warm");
+  double* d = nullptr;
+  TRY(dalloc(&d, size_t(c->nstore) * c->K));
+  CU(cudaStreamSynchronize(c->cs));
+  DevState h;
+  CU(cudaMemcpy(&h, c->st, sizeof(h), cudaMemcpyDeviceToHost));
+  warm_read<<<592, 256, 0, c->cs>>>(c->U, c->T, c->P, c->nstore, c->K, uint32_t(h.commits), d);
+  CU(cudaStreamSynchronize(c->cs));
+  CU(cudaMemcpy(warm_h, d, size_t(c->nstore) * c->K * sizeof(double), cudaMemcpyDeviceToHost));
+  dfree(d);
+  return 0;
+}
+
+int isnmf_online_enqueue(isnmf_online* c, const float* frames, int64_t ldv, int64_t n, const uint64_t* index,
+                         uint64_t budget, double eta) {
+  if (!c) return fail(ISNMF_E_INVALID_ARG, "NULL context");
+  return online_enqueue(c, frames, ldv, n, index, budget, eta);
+}
+
+int isnmf_online_synchronize(isnmf_online* c) {
+  if (!c) return fail(ISNMF_E_INVALID_ARG, "NULL context");
+  return online_finish(c, nullptr);
+}
+
+int isnmf_online_run(isnmf_online* c, const float* frames, int64_t ldv, int64_t n, const uint64_t* index,
+                     uint64_t budget, double eta, int32_t* stopped) {
+  if (!c) return fail(ISNMF_E_INVALID_ARG, "NULL context");
+  int rc = online_enqueue(c, frames, ldv, n, index, budget, eta);
+  int rc2 = online_finish(c, stopped);
+  return rc ? rc : rc2;
+}
+
+int isnmf_online_get_trace(isnmf_online* c, uint64_t* samples, double* obj, double* seconds, int64_t cap,
+                           int64_t* n) {
+  if (!c) return fail(ISNMF_E_INVALID_ARG, "NULL context");
+  DevState h;
+  TRY(read_state(c, &h));
+  const int64_t cnt = std::min<int64_t>(int64_t(h.commits - h.trace_base), std::min<int64_t>(cap, c->tr_cap));
+  if (n) *n = std::max<int64_t>(cnt, 0);
+  if (cnt <= 0) return 0;
+  std::vector<unsigned long long> t(static_cast<size_t>(cnt)), ns(static_cast<size_t>(cnt));
+  std::vector<double> o(static_cast<size_t>(cnt));
+  CU(cudaMemcpy(t.data(), c->tr_t, cnt * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(ns.data(), c->tr_ns, cnt * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(o.data(), c->tr_obj, cnt * sizeof(double), cudaMemcpyDeviceToHost));
+  for (int64_t i = 0; i < cnt; ++i) {
+    if (samples) samples[i] = t[size_t(i)];
+    if (obj) obj[i] = o[size_t(i)];
+    if (seconds) seconds[i] = double(ns[size_t(i)] - h.origin_ns) * 1e-9;
+  }
+  return 0;
+}
+
+int isnmf_online_clear_trace(isnmf_online* c) {
+  if (!c) return fail(ISNMF_E_INVALID_ARG, "NULL context");
+  DevState h;
+  TRY(read_state(c, &h));
+  h.trace_base = h.commits;
+  CU(cudaMemcpy(c->st, &h, sizeof(h), cudaMemcpyHostToDevice));
+  c->trace_base = h.commits;
+  mark_origin<<<1, 1, 0, c->cs>>>(c->st);
+  CU(cudaStreamSynchronize(c->cs));
+  return 0;
+}
+
+int isnmf_online_get_last_h(isnmf_online* c, double* h, int64_t n) {
+  if (!c || !h) return fail(ISNMF_E_INVALID_ARG, "NULL argument");
+  if (n < 0 || n > c->beta) return fail(ISNMF_E_INVALID_ARG, "get_last_h: n must be <= beta");
+  std::vector<float> tmp(size_t(n) * c->K);
+  CU(cudaStreamSynchronize(c->cs));
+  CU(cudaMemcpy(tmp.data(), c->Hlast, tmp.size() * sizeof(float), cudaMemcpyDeviceToHost));
+  for (size_t i = 0; i < tmp.size(); ++i) h[i] = tmp[i];
+  return 0;
+}
+
+int64_t isnmf_online_launch_count(isnmf_online* c) { return c ? c->launches : -1; }
+
+int isnmf_online_profile_begin(isnmf_online* c) {
+  if (!c) return fail(ISNMF_E_INVALID_ARG, "NULL context");
+  for (int i = 0; i < 2; ++i)
+    if (!c->ev_span[i]) CU(cudaEventCreate(&c->ev_span[i]));
+  c->prof = true;
+  c->ev_used = 0;
+  c->prof_frames = 0;
+  CU(cudaEventRecord(c->ev_span[0], c->cs));
+  return 0;
+}
+
+int isnmf_online_profile_end(isnmf_online* c, double* solve_ms, int64_t* solve_launches, int64_t* solve_frames,
+                             double* span_ms) {
+  if (!c || !c->prof) return fail(ISNMF_E_INVALID_ARG, "profile_end without profile_begin");
+  CU(cudaEventRecord(c->ev_span[1], c->cs));
+  CU(cudaEventSynchronize(c->ev_span[1]));
+  double tot = 0.0;
+  for (size_t i = 0; i + 1 < c->ev_used; i += 2) {
+    float ms = 0.0f;
+    CU(cudaEventElapsedTime(&ms, c->ev_pool[i], c->ev_pool[i + 1]));
+    tot += ms;
+  }
+  float span = 0.0f;
+  CU(cudaEventElapsedTime(&span, c->ev_span[0], c->ev_span[1]));
+  if (solve_ms) *solve_ms = tot;
+  if (solve_launches) *solve_launches = int64_t(c->ev_used / 2);
+  if (solve_frames) *solve_frames = c->prof_frames;
+  if (span_ms) *span_ms = span;
+  c->prof = false;
+  return 0;
+}
+
+}  // extern "C"
+
+// ===========================================================================
+// Stateless kernels (kernels.hpp) and the batch trainer (batch.hpp)
+// ===========================================================================
+namespace {
+
+__global__ void is_div_kernel(const double* y, const double* x, int64_t n, double eps, double* out) {
+  __shared__ double sh[256];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += is_term_d((y[i] - x[i]) / (eps + x[i]));
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = sh[0];
+}
+
+__global__ void update_w_kernel(const double* a, const double* b, const double* wp, int64_t n, double* w,
+                                unsigned int* status) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    if (b[i] > 0.0)
+      w[i] = sqrt(a[i] / b[i]);
+    else if (a[i] > 0.0)
+      atomicOr(status, ST_INCONSISTENT);
+    else
+      w[i] = wp[i];
+  }
+}
+
+// model.hpp:73-86 on column-major W/A/B (F x K) and optional warm_h (K x N).
+__global__ void rescale_kernel(double* w, double* a, double* b, int64_t F, int64_t K, double* h, int64_t N,
+                               unsigned int* status) {
+  const int64_t k = blockIdx.x;
+  __shared__ double sh[256];
+  double s = 0.0;
+  for (int64_t f = threadIdx.x; f < F; f += blockDim.x) s += w[k * F + f];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    __syncthreads();
+  }
+  const double sc = sh[0];
+  if (!(sc > 0.0)) {
+    if (threadIdx.x == 0) atomicOr(status, ST_ZERO_COLUMN);
+    return;
+  }
+  for (int64_t f = threadIdx.x; f < F; f += blockDim.x) {
+    w[k * F + f] /= sc;
+    a[k * F + f] /= sc;
+    b[k * F + f] *= sc;
+  }
+  if (h)
+    for (int64_t n = threadIdx.x; n < N; n += blockDim.x) h[n * K + k] *= sc;
+}
+
+// A device workspace for the fused solve over an arbitrary set of frames.
+struct SolveWork {
+  int F = 0, K = 0, WS = 0, KP = 0, NT = 0;
+  Variant* var = nullptr;
+  size_t smem = 0;
+  int seg_blocks = 0;
+  cudaStream_t s = nullptr;
+  DevState* st = nullptr;
+  float* W32 = nullptr;
+  double* W64 = nullptr;
+  double *pa = nullptr, *pb = nullptr, *A = nullptr, *B = nullptr, *Wtmp = nullptr, *colpart = nullptr;
+  double *P = nullptr, *scale = nullptr;
+  float* stats = nullptr;
+  double* divpart = nullptr;
+  unsigned int* halt = nullptr;
+
+  ~SolveWork() {
+    if (s) cudaStreamSynchronize(s);
+    void* ptrs[] = {st, W32, W64, pa, pb, A, B, Wtmp, colpart, P, scale, stats, divpart, halt};
+    for (void* p : ptrs) dfree(p);
+    if (s) cudaStreamDestroy(s);
+  }
+
+  int init(int64_t F_, int64_t K_, int64_t frames) {
+    F = int(F_);
+    K = int(K_);
+    TRY(pick_variant(F, K, frames, &var, &WS, &smem));
+    KP = 4 * var->TK;
+    NT = 4 * var->TN;
+    seg_blocks = device_sms() * 4;
+    CU(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    const size_t FK = size_t(F) * K;
+    TRY(dalloc(&st, 1));
+    TRY(dalloc(&W32, size_t(F) * WS));
+    TRY(dalloc(&W64, FK));
+    TRY(dalloc(&pa, FK));
+    TRY(dalloc(&pb, FK));
+    TRY(dalloc(&A, FK));
+    TRY(dalloc(&B, FK));
+    TRY(dalloc(&Wtmp, FK));
+    TRY(dalloc(&colpart, 2 * size_t(K)));
+    TRY(dalloc(&P, 2 * size_t(K)));
+    TRY(dalloc(&scale, size_t(K)));
+    TRY(dalloc(&stats, size_t(seg_blocks) * 2 * F * KP));
+    TRY(dalloc(&divpart, size_t(seg_blocks)));
+    TRY(dalloc(&halt, 1));
+    CU(cudaMemset(halt, 0, sizeof(unsigned int)));
+    CU(cudaMemset(pa, 0, FK * sizeof(double)));
+    CU(cudaMemset(pb, 0, FK * sizeof(double)));
+    CU(cudaMemset(A, 0, FK * sizeof(double)));
+    CU(cudaMemset(B, 0, FK * sizeof(double)));
+    DevState h{};
+    h.last_delta = INFINITY;
+    CU(cudaMemcpy(st, &h, sizeof(h), cudaMemcpyHostToDevice));
+    return 0;
+  }
+
+  // W from host column-major fp64 (F x K)
+  int set_w(const double* w) {
+    std::vector<double> rm(size_t(F) * K);
+    to_rowmajor(w, F, K, rm.data());
+    CU(cudaMemcpy(W64, rm.data(), rm.size() * sizeof(double), cudaMemcpyHostToDevice));
+    std::vector<float> w32(size_t(F) * WS, 0.0f);
+    for (int64_t k = 0; k < K; ++k)
+      for (int64_t f = 0; f < F; ++f) w32[f * WS + k] = float(w[k * F + f]);
+    CU(cudaMemcpy(W32, w32.data(), w32.size() * sizeof(float), cudaMemcpyHostToDevice));
+    return 0;
+  }
+
+  // One fused pass over frames [0, n) of V (device, ld ldv): h0 from H (device
+  // [n][K]) scaled by hscale, `iters` MM iterations, H written back in place;
+  // statistics reduced into pa/pb and the divergence into st->pending_div.
+  int pass(const float* V, int64_t ldv, int64_t n, float* H, int iters, double eps, const double* hscale,
+           bool stats_on, bool div_first, bool check_h0) {
+    for (int64_t s0 = 0; s0 < n; s0 += int64_t(seg_blocks) * NT) {
+      const int64_t ns = std::min<int64_t>(n - s0, int64_t(seg_blocks) * NT);
+      const int nblk = int((ns + NT - 1) / NT);
+      SolveArgs a{};
+      a.W32 = W32;
+      a.F = F;
+      a.K = K;
+      a.WS = WS;
+      a.V = V;
+      a.ldv = ldv;
+      a.v0 = s0;
+      a.nframes = int(ns);
+      a.iters = iters;
+      a.eps = float(eps);
+      a.epsd = eps;
+      a.h0_mode = 0;
+      a.H0 = H + s0 * K;
+      a.hscale = hscale;
+      a.Hout = H + s0 * K;
+      a.check_h0 = check_h0;
+      a.do_stats = 1;
+      a.div_first = div_first;
+      a.stats = stats_on ? stats : nullptr;
+      a.divpart = divpart;
+      a.status = &st->status;
+      a.halt = halt;
+      var->fn<<<nblk, kThreads, smem, s>>>(a);
+      ReduceArgs r{};
+      r.stats = stats;
+      r.divpart = divpart;
+      r.nblk = stats_on ? nblk : 0;
+      r.F = F;
+      r.K = K;
+      r.KP = KP;
+      r.nframes = int(ns);
+      r.W64 = W64;
+      r.pa = pa;
+      r.pb = pb;
+      r.do_commit = 0;
+      r.st = st;
+      r.halt = halt;
+      if (!stats_on) {  // divergence only: fold divpart with a 1-thread reduce
+        r.F = 0;
+        r.nblk = 0;
+      }
+      // divergence partials are always folded (reduce_kernel block 0 sums divpart[0..nblk_div))
+      r.nblk = nblk;
+      if (!stats_on) r.F = 0;
+      reduce_kernel<<<std::max(1, (r.F * K + 255) / 256), 256, 0, s>>>(r);
+      CU(cudaGetLastError());
+    }
+    return 0;
+  }
+
+  int state(DevState* h) {
+    CU(cudaStreamSynchronize(s));
+    CU(cudaMemcpy(h, st, sizeof(DevState), cudaMemcpyDeviceToHost));
+    return 0;
+  }
+};
+
+int upload_frames(const double* v, int64_t F, int64_t N, float** dv) {
+  std::vector<float> v32(size_t(F) * N);
+  for (size_t i = 0; i < v32.size(); ++i) v32[i] = float(v[i]);
+  TRY(dalloc(dv, v32.size()));
+  CU(cudaMemcpy(*dv, v32.data(), v32.size() * sizeof(float), cudaMemcpyHostToDevice));
+  return 0;
+}
+
+int upload_h(const double* h, int64_t K, int64_t N, float** dh) {
+  std::vector<float> h32(size_t(K) * N);
+  for (size_t i = 0; i < h32.size(); ++i) h32[i] = float(h[i]);
+  TRY(dalloc(dh, std::max<size_t>(1, h32.size())));
+  if (!h32.empty()) CU(cudaMemcpy(*dh, h32.data(), h32.size() * sizeof(float), cudaMemcpyHostToDevice));
+  return 0;
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  ~DevBuf() { dfree(p); }
+};
+
+}  // namespace
+
+extern "C" {
+
+int isnmf_is_divergence(const double* y, int64_t ny, const double* x, int64_t nx, double eps, double* out) {
+  if (!out) return fail(ISNMF_E_INVALID_ARG, "NULL out");
+  if (ny != nx) return fail(ISNMF_E_SHAPE_MISMATCH, "is_divergence: %lld vs %lld", (long long)ny, (long long)nx);
+  if (!(eps > 0.0)) return fail(ISNMF_E_NEGATIVE_INPUT, "epsilon must be > 0");
+  for (int64_t i = 0; i < ny; ++i)
+    if (y[i] < 0.0 || x[i] < 0.0) return fail(ISNMF_E_NEGATIVE_INPUT, "is_divergence: negative entry");
+  DevBuf dy, dx, dout;
+  TRY(dalloc(reinterpret_cast<double**>(&dy.p), ny));
+  TRY(dalloc(reinterpret_cast<double**>(&dx.p), ny));
+  TRY(dalloc(reinterpret_cast<double**>(&dout.p), 1));
+  if (ny) {
+    CU(cudaMemcpy(dy.p, y, ny * sizeof(double), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(dx.p, x, ny * sizeof(double), cudaMemcpyHostToDevice));
+  }
+  is_div_kernel<<<1, 256>>>(static_cast<double*>(dy.p), static_cast<double*>(dx.p), ny, eps,
+                            static_cast<double*>(dout.p));
+  CU(cudaGetLastError());
+  CU(cudaMemcpy(out, dout.p, sizeof(double), cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+static int stateless(const double* v, const double* w, const double* h, int64_t F, int64_t K, int64_t N, int iters,
+                     double eps, bool stats, bool check_h0, double* h_out, double* a_out, double* b_out,
+                     double* div_out) {
+  if (!v || !w || !h) return fail(ISNMF_E_INVALID_ARG, "NULL input");
+  if (!(eps > 0.0)) return fail(ISNMF_E_NEGATIVE_INPUT, "epsilon must be > 0");
+  if (F < 1 || K < 1 || N < 0) return fail(ISNMF_E_SHAPE_MISMATCH, "inconsistent shapes");
+  SolveWork wk;
+  TRY(wk.init(F, K, std::max<int64_t>(N, 1)));
+  TRY(wk.set_w(w));
+  float *dv = nullptr, *dh = nullptr;
+  TRY(upload_frames(v, F, N, &dv));
+  DevBuf bv, bh;
+  bv.p = dv;
+  TRY(upload_h(h, K, N, &dh));
+  bh.p = dh;
+  TRY(wk.pass(dv, F, N, dh, iters, eps, nullptr, stats, false, check_h0));
+  DevState st;
+  TRY(wk.state(&st));
+  if (st.status) return status_to_code(st.status, "solve_h", 0);
+  if (h_out) {
+    std::vector<float> h32(size_t(K) * N);
+    if (N) CU(cudaMemcpy(h32.data(), dh, h32.size() * sizeof(float), cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < h32.size(); ++i) h_out[i] = h32[i];
+  }
+  if (a_out || b_out) {
+    std::vector<double> rm(size_t(F) * K);
+    if (a_out) {
+      CU(cudaMemcpy(rm.data(), wk.pa, rm.size() * sizeof(double), cudaMemcpyDeviceToHost));
+      to_colmajor(rm.data(), F, K, a_out);
+    }
+    if (b_out) {
+      CU(cudaMemcpy(rm.data(), wk.pb, rm.size() * sizeof(double), cudaMemcpyDeviceToHost));
+      to_colmajor(rm.data(), F, K, b_out);
+    }
+  }
+  if (div_out) *div_out = st.pending_div;
+  return 0;
+}
+
+int isnmf_objective(const double* v, const double* w, const double* h, int64_t F, int64_t K, int64_t N, double eps,
+                    double* out) {
+  if (!out) return fail(ISNMF_E_INVALID_ARG, "NULL out");
+  if (N == 0) return fail(ISNMF_E_EMPTY_DATASET, "objective: no columns");
+  double d = 0.0;
+  TRY(stateless(v, w, h, F, K, N, 0, eps, false, false, nullptr, nullptr, nullptr, &d));
+  *out = d / double(N);
+  return 0;
+}
+
+int isnmf_solve_h(const double* v, const double* w, const double* h0, int64_t F, int64_t K, int64_t N, int iters,
+                  double eps, double* h_out) {
+  if (!h_out) return fail(ISNMF_E_INVALID_ARG, "NULL out");
+  if (iters < 0) return fail(ISNMF_E_NEGATIVE_INPUT, "solve_h: iters < 0");
+  for (int64_t i = 0; i < K * N; ++i)
+    if (!(h0[i] > 0.0)) return fail(ISNMF_E_NON_POSITIVE_INIT, "solve_h: h0 must be positive");
+  return stateless(v, w, h0, F, K, N, iters, eps, false, true, h_out, nullptr, nullptr, nullptr);
+}
+
+int isnmf_batch_stats(const double* v, const double* w, const double* h, int64_t F, int64_t K, int64_t N, double eps,
+                      double* a_out, double* b_out) {
+  if (!a_out || !b_out) return fail(ISNMF_E_INVALID_ARG, "NULL out");
+  return stateless(v, w, h, F, K, N, 0, eps, true, false, nullptr, a_out, b_out, nullptr);
+}
+
+int isnmf_update_w(const double* a, const double* b, const double* w_prev, int64_t F, int64_t K, double* w_out) {
+  if (!a || !b || !w_prev || !w_out) return fail(ISNMF_E_INVALID_ARG, "NULL argument");
+  const int64_t n = F * K;
+  DevBuf da, db, dw, dout, dst;
+  TRY(dalloc(reinterpret_cast<double**>(&da.p), n));
+  TRY(dalloc(reinterpret_cast<double**>(&db.p), n));
+  TRY(dalloc(reinterpret_cast<double**>(&dw.p), n));
+  TRY(dalloc(reinterpret_cast<double**>(&dout.p), n));
+  TRY(dalloc(reinterpret_cast<unsigned int**>(&dst.p), 1));
+  CU(cudaMemset(dst.p, 0, sizeof(unsigned int)));
+  CU(cudaMemcpy(da.p, a, n * sizeof(double), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(db.p, b, n * sizeof(double), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(dw.p, w_prev, n * sizeof(double), cudaMemcpyHostToDevice));
+  update_w_kernel<<<std::max<int64_t>(1, std::min<int64_t>(1184, (n + 255) / 256)), 256>>>(
+      static_cast<double*>(da.p), static_cast<double*>(db.p), static_cast<double*>(dw.p), n,
+      static_cast<double*>(dout.p), static_cast<unsigned int*>(dst.p));
+  CU(cudaGetLastError());
+  unsigned int stt = 0;
+  CU(cudaMemcpy(&stt, dst.p, sizeof(stt), cudaMemcpyDeviceToHost));
+  if (stt) return status_to_code(stt, "update_w", 0);
+  CU(cudaMemcpy(w_out, dout.p, n * sizeof(double), cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+int isnmf_rescale_dictionary(double* w, double* a, double* b, int64_t F, int64_t K, double* warm_h, int64_t N) {
+  if (!w || !a || !b) return fail(ISNMF_E_INVALID_ARG, "NULL argument");
+  const int64_t n = F * K;
+  DevBuf dw, da, db, dh, dst;
+  TRY(dalloc(reinterpret_cast<double**>(&dw.p), n));
+  TRY(dalloc(reinterpret_cast<double**>(&da.p), n));
+  TRY(dalloc(reinterpret_cast<double**>(&db.p), n));
+  TRY(dalloc(reinterpret_cast<unsigned int**>(&dst.p), 1));
+  CU(cudaMemset(dst.p, 0, sizeof(unsigned int)));
+  CU(cudaMemcpy(dw.p, w, n * sizeof(double), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(da.p, a, n * sizeof(double), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(db.p, b, n * sizeof(double), cudaMemcpyHostToDevice));
+  if (warm_h) {
+    TRY(dalloc(reinterpret_cast<double**>(&dh.p), K * N));
+    if (K * N) CU(cudaMemcpy(dh.p, warm_h, K * N * sizeof(double), cudaMemcpyHostToDevice));
+  }
+  if (K > 0)
+    rescale_kernel<<<int(K), 256>>>(static_cast<double*>(dw.p), static_cast<double*>(da.p),
+                                    static_cast<double*>(db.p), F, K, static_cast<double*>(dh.p), N,
+                                    static_cast<unsigned int*>(dst.p));
+  CU(cudaGetLastError());
+  unsigned int stt = 0;
+  CU(cudaMemcpy(&stt, dst.p, sizeof(stt), cudaMemcpyDeviceToHost));
+  if (stt) return status_to_code(stt, "rescale_dictionary", 0);
+  CU(cudaMemcpy(w, dw.p, n * sizeof(double), cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(a, da.p, n * sizeof(double), cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(b, db.p, n * sizeof(double), cudaMemcpyDeviceToHost));
+  if (warm_h && K * N) CU(cudaMemcpy(warm_h, dh.p, K * N * sizeof(double), cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+// batch_train (batch.hpp:84-143).  Per epoch e: one fused pass (objective of
+// the incoming (W, H) from the first Lambda, one MM update of every column of
+// H, statistics of the updated H), then W = sqrt(A/B) and the l1 rescale whose
+// column scales multiply H on the next read.  The objective of epoch e is thus
+// measured during epoch e+1's pass (shared Lambda, 12FKN per epoch instead of
+// the reference's 14FKN); a final divergence-only pass closes the last epoch.
+int isnmf_batch_train(const float* v, int64_t ldv, int64_t F, int64_t N, int64_t K, const double* w0,
+                      const double* h0, uint64_t max_epochs, double eps, double eta, double* w_out, double* h_out,
+                      double* obj_trace, uint64_t* epochs, double* initial_obj, double* last_delta) {
+  if (!v || !w0 || !h0 || !w_out || !h_out) return fail(ISNMF_E_INVALID_ARG, "NULL argument");
+  if (N == 0) return fail(ISNMF_E_EMPTY_DATASET, "batch_train: empty dataset");
+  if (F < 1 || K < 1 || ldv < F) return fail(ISNMF_E_SHAPE_MISMATCH, "batch_train: inconsistent V/W0/H0 shapes");
+  if (!(eps > 0.0)) return fail(ISNMF_E_NEGATIVE_INPUT, "config: epsilon must be > 0");
+  for (int64_t i = 0; i < F * K; ++i)
+    if (!(w0[i] > 0.0)) return fail(ISNMF_E_NON_POSITIVE_INIT, "batch_train: w0 and h0 must be strictly positive");
+  for (int64_t i = 0; i < K * N; ++i)
+    if (!(h0[i] > 0.0)) return fail(ISNMF_E_NON_POSITIVE_INIT, "batch_train: w0 and h0 must be strictly positive");
+  SolveWork wk;
+  TRY(wk.init(F, K, N));
+  TRY(wk.set_w(w0));
+  DevBuf bv, bh, bs;
+  const float* dv = v;
+  int64_t dld = ldv;
+  if (!is_device_ptr(v)) {
+    float* tmp = nullptr;
+    TRY(dalloc(&tmp, size_t(F) * N));
+    CU(cudaMemcpy2D(tmp, size_t(F) * sizeof(float), v, size_t(ldv) * sizeof(float), size_t(F) * sizeof(float),
+                    size_t(N), cudaMemcpyHostToDevice));
+    bv.p = tmp;
+    dv = tmp;
+    dld = F;
+  }
+  float* dh = nullptr;
+  TRY(upload_h(h0, K, N, &dh));
+  bh.p = dh;
+  double* dscale = nullptr;  // rescale factors to apply on the next H read
+  TRY(dalloc(&dscale, size_t(K)));
+  bs.p = dscale;
+  fill_f64<<<1, 256, 0, wk.s>>>(dscale, K, 1.0);
+  fill_f64<<<1, 256, 0, wk.s>>>(wk.P, 2 * K, 1.0);
+  const double dK = double(K);
+  (void)dK;
+  double prev = 0.0;
+  uint64_t done = 0;
+  double delta = 0.0;
+  for (uint64_t e = 1; e <= max_epochs; ++e) {
+    // reset per-epoch accumulators
+    CU(cudaMemsetAsync(wk.pa, 0, size_t(F) * K * sizeof(double), wk.s));
+    CU(cudaMemsetAsync(wk.pb, 0, size_t(F) * K * sizeof(double), wk.s));
+    {
+      DevState h{};
+      TRY(wk.state(&h));
+      if (h.status) return status_to_code(h.status, "batch_train", 0);
+      h.pending_div = 0.0;
+      h.pending_count = 0;
+      CU(cudaMemcpy(wk.st, &h, sizeof(h), cudaMemcpyHostToDevice));
+    }
+    TRY(wk.pass(dv, dld, N, dh, 1, eps, dscale, true, true, false));
+    // elementwise commit with rho = 0: A = stats, B = stats, Wtmp = sqrt(A/B)
+    ReduceArgs r{};
+    r.stats = wk.stats;
+    r.divpart = wk.divpart;
+    r.nblk = 0;
+    r.F = int(F);
+    r.K = int(K);
+    r.KP = wk.KP;
+    r.nframes = 0;
+    r.W64 = wk.W64;
+    r.pa = wk.pa;
+    r.pb = wk.pb;
+    r.A = wk.A;
+    r.B = wk.B;
+    r.Wtmp = wk.Wtmp;
+    r.do_commit = 1;
+    r.rho = 0.0;
+    r.st = wk.st;
+    r.halt = wk.halt;
+    reduce_kernel<<<int((F * K + 255) / 256), 256, 0, wk.s>>>(r);
+    CommitArgs m{};
+    m.F = int(F);
+    m.K = int(K);
+    m.WS = wk.WS;
+    m.Wtmp = wk.Wtmp;
+    m.W64 = wk.W64;
+    m.A = wk.A;
+    m.B = wk.B;
+    m.W32 = wk.W32;
+    m.P = wk.P;
+    m.colpart = wk.colpart;
+    m.st = wk.st;
+    m.halt = wk.halt;
+    m.scale_out = dscale;
+    m.batch_mode = 1;
+    // commit_kernel indexes P by st->commits: keep commits at 0 (2-row P)
+    commit_kernel<<<int(K), 256, 0, wk.s>>>(m);
+    CU(cudaGetLastError());
+    DevState h{};
+    TRY(wk.state(&h));
+    if (h.status) return status_to_code(h.status, "batch_train", e);
+    const double obj_prev = h.last_obj;  // objective of (W_{e-1}, H_{e-1})
+    if (e == 1) {
+      prev = obj_prev;
+      if (initial_obj) *initial_obj = obj_prev;
+    } else {
+      if (obj_prev > prev + 1e-6 * prev + 1e-15)
+        return fail(ISNMF_E_DIVERGED_OBJECTIVE, "batch_train: objective increased at epoch %llu",
+                    (unsigned long long)(e - 1));
+      prev = obj_prev;
+      if (obj_trace) obj_trace[e - 2] = obj_prev;
+    }
+    h.commits = 0;  // P stays 2 rows
+    CU(cudaMemcpy(wk.st, &h, sizeof(h), cudaMemcpyHostToDevice));
+    delta = h.last_delta;
+    done = e;
+    if (delta < eta) break;
+  }
+  // final objective of (W_e, H_e): divergence-only pass that also applies the last rescale to H
+  {
+    DevState h{};
+    TRY(wk.state(&h));
+    h.pending_div = 0.0;
+    h.pending_count = 0;
+    CU(cudaMemcpy(wk.st, &h, sizeof(h), cudaMemcpyHostToDevice));
+    TRY(wk.pass(dv, dld, N, dh, 0, eps, dscale, false, false, false));
+    TRY(wk.state(&h));
+    if (h.status) return status_to_code(h.status, "batch_train", done);
+    const double obj = h.pending_div / double(N);
+    if (done >= 1) {
+      if (obj > prev + 1e-6 * prev + 1e-15)
+        return fail(ISNMF_E_DIVERGED_OBJECTIVE, "batch_train: objective increased at epoch %llu",
+                    (unsigned long long)done);
+      if (obj_trace) obj_trace[done - 1] = obj;
+    } else if (initial_obj) {
+      *initial_obj = obj;
+    }
+  }
+  std::vector<double> rm(size_t(F) * K);
+  CU(cudaMemcpy(rm.data(), wk.W64, rm.size() * sizeof(double), cudaMemcpyDeviceToHost));
+  to_colmajor(rm.data(), F, K, w_out);
+  std::vector<float> h32(size_t(K) * N);
+  CU(cudaMemcpy(h32.data(), dh, h32.size() * sizeof(float), cudaMemcpyDeviceToHost));
+  for (size_t i = 0; i < h32.size(); ++i) h_out[i] = h32[i];
+  if (epochs) *epochs = done;
+  if (last_delta) *last_delta = delta;
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,721 @@
+// Device kernels of the B200 online / batch IS-NMF engine (sm_100a).
+//
+// K1  solve_kernel   — fused mini-batch H solver (kernels.hpp:62-80) with the
+//                      statistics epilogue (kernels.hpp:95-108, online.hpp:360-361)
+//                      and the IS-divergence of the final fit (online.hpp:303-309).
+// K2  reduce_kernel  — deterministic fixed-order reduction of the per-CTA A/B
+//                      partials into pending (online.hpp:360-361) and the
+//                      elementwise half of dictionary_commit (online.hpp:319-325,
+//                      update_w kernels.hpp:142-159).
+// K3  commit_kernel  — per-column half of the commit: l1 renormalisation
+//                      (model.hpp:73-86), ||dW||_F (matrix.hpp:38-41), trace
+//                      point and eta stop rule (online.hpp:328-336, 390-396).
+// K0  fresh_kernel   — reference fresh-restart uniforms: std::mt19937_64 seeded
+//                      with splitmix64(mix_seed(seed, t)) (online.hpp:294-301,
+//                      rng.hpp:10-34), bit-exact.
+//
+// Layout in HBM (row-major [F][K] for the fp64 state so the reduce kernel is
+// coalesced; W32 is the solver's fp32 copy with row stride WS >= K padded with
+// zero columns).  See DESIGN.md for the roofline of each kernel.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace isnmf_dev {
+
+constexpr int kWarps = 8;
+constexpr int kThreads = kWarps * 32;
+constexpr int kChunk = 32;  // rows of F per warp chunk
+constexpr int kQS = 68;     // floats per Q/R staging row: [nd 2][ng 4][8] + 4 skew
+
+enum : uint32_t {
+  ST_NONPOS_INIT = 1u,
+  ST_INCONSISTENT = 2u,
+  ST_NONFINITE_W = 4u,
+  ST_ZERO_COLUMN = 8u,
+  ST_DIVERGED = 16u,
+};
+
+// Device-resident scalar state of an online / batch context.
+struct DevState {
+  unsigned long long t;              // samples seen (online.hpp:226)
+  unsigned long long commits;        // online.hpp:234
+  unsigned long long pending_count;  // online.hpp:239
+  unsigned long long trace_base;     // commits at the last trace clear
+  unsigned long long origin_ns;      // clock origin for trace seconds
+  double pending_div;                // online.hpp:238
+  double last_delta;                 // online.hpp:233
+  double last_obj;                   // online.hpp:240
+  double kmeanw;                     // K * mean(W) (fresh_h_init, online.hpp:296-297)
+  double prev_obj;                   // batch: previous objective (batch.hpp:129)
+  unsigned int status;               // error bits (ST_*)
+  unsigned int halt;                 // eta stop rule fired
+  unsigned int ticket;               // last-block-done counter of commit_kernel
+  unsigned int pad;
+};
+
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// is_term (kernels.hpp:15-18) in fp32, taking ratio = 1 + u = (v+eps)/lam
+// computed as a product: a series for |u| < 1/4 (where u - log1p(u) cancels),
+// u - log(ratio) elsewhere, so ratios far below 1 (v at the 1e-9 floor) keep
+// full relative accuracy instead of rounding u to -1.  Relative error <~1e-6.
+__device__ __forceinline__ float is_term_ratio(float ratio) {
+  const float u = ratio - 1.0f;
+  if (fabsf(u) < 0.25f) {
+    float p = -1.0f / 12.0f;
+    p = fmaf(p, u, 1.0f / 11.0f);
+    p = fmaf(p, u, -1.0f / 10.0f);
+    p = fmaf(p, u, 1.0f / 9.0f);
+    p = fmaf(p, u, -1.0f / 8.0f);
+    p = fmaf(p, u, 1.0f / 7.0f);
+    p = fmaf(p, u, -1.0f / 6.0f);
+    p = fmaf(p, u, 1.0f / 5.0f);
+    p = fmaf(p, u, -1.0f / 4.0f);
+    p = fmaf(p, u, 1.0f / 3.0f);
+    p = fmaf(p, u, -1.0f / 2.0f);
+    return -(u * u) * p;
+  }
+  const float t = u - logf(ratio);
+  return t > 0.0f ? t : 0.0f;
+}
+
+__device__ __forceinline__ double is_term_d(double u) {
+  const double t = u - log1p(u);
+  return t > 0.0 ? t : 0.0;
+}
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ---------------------------------------------------------------------------
+// K1 — fused solve.
+// ---------------------------------------------------------------------------
+struct SolveArgs {
+  const float* W32;  // [F][WS]
+  int F, K, WS;
+  const float* V;  // frames; block-local frame n is V + frame(n) * ldv
+  int64_t ldv;
+  const int64_t* vsel;  // frame(n) = vsel[n] (nullable)
+  int64_t v0;           // frame(n) = v0 + n when vsel == nullptr
+  int nframes;
+  int iters;
+  float eps;
+  double epsd;
+  int h0_mode;  // 0 direct H0, 1 warm store (U, T, P), 2 fresh (u01, kmeanw)
+  const float* H0;
+  float* U;
+  uint32_t* T;
+  const double* P;
+  uint32_t c_now;
+  const uint64_t* widx;  // store column of frame n (nullable -> (wbase + n) mod wmod)
+  int64_t wbase;
+  int64_t wmod;
+  const double* u01;
+  const DevState* kst;  // kmeanw for fresh
+  const double* hscale;  // optional per-k multiplier on h0 (batch rescale)
+  float* Hout;           // [nframes][K] (nullable)
+  int write_store;
+  int do_stats;   // extra pass with the final h: divergence (+ statistics when stats != nullptr)
+  int div_first;  // divergence from pass 0 (the incoming h) instead of the final pass
+  int check_h0;   // flag h0 <= 0 as NonPositiveInit (solve_h, kernels.hpp:67)
+  float* stats;     // [gridDim][2][F][KP]
+  double* divpart;  // [gridDim]
+  unsigned int* status;
+  const unsigned int* halt;
+};
+
+template <int TK>
+struct KMap {
+  static constexpr int M = TK / 4;
+  static constexpr int TT = TK - 4 * M;
+  __host__ __device__ static constexpr int k_of(int kg, int j) {
+    return j < 4 * M ? 4 * (4 * (j / 4) + kg) + (j & 3) : 16 * M + kg * TT + (j - 4 * M);
+  }
+  __host__ __device__ static constexpr void inv(int k, int& kg, int& j) {
+    if (k < 16 * M) {
+      const int c = k >> 2;
+      kg = c & 3;
+      j = 4 * (c >> 2) + (k & 3);
+    } else {
+      const int off = k - 16 * M;
+      kg = off / (TT > 0 ? TT : 1);
+      j = 4 * M + off % (TT > 0 ? TT : 1);
+    }
+  }
+};
+
+template <int TK, int TN>
+struct SolveShape {
+  static constexpr int KP = 4 * TK;
+  static constexpr int NT = 4 * TN;
+  static constexpr int cells = TK * TN;
+  static constexpr int pbs0 = (cells + 3) / 4 * 4;
+  static constexpr int PBS = ((pbs0 / 4) % 2 == 0) ? pbs0 + 4 : pbs0;  // 16B-aligned, odd # of float4s
+  static constexpr int union_floats =
+      (kWarps * kChunk * kQS > kWarps * 32 * PBS) ? kWarps * kChunk * kQS : kWarps * 32 * PBS;
+  static size_t smem_bytes(int F, int WS) { return sizeof(float) * (size_t(F) * WS + NT * KP + union_floats); }
+};
+
+// Loads the lane's TK dictionary values of one row (k-set of group kg).
+template <int TK>
+__device__ __forceinline__ void load_wk(const float* wr, int kg, float (&w)[TK]) {
+  using KM = KMap<TK>;
+#pragma unroll
+  for (int q = 0; q < KM::M; ++q) {
+    const float4 t = *reinterpret_cast<const float4*>(wr + 4 * (4 * q + kg));
+    w[4 * q + 0] = t.x;
+    w[4 * q + 1] = t.y;
+    w[4 * q + 2] = t.z;
+    w[4 * q + 3] = t.w;
+  }
+#pragma unroll
+  for (int e = 0; e < KM::TT; ++e) w[4 * KM::M + e] = wr[16 * KM::M + kg * KM::TT + e];
+}
+
+template <int TN>
+__device__ __forceinline__ void load_x(const float* xr, float (&x)[TN]) {
+  if constexpr (TN >= 4) {
+    const float4 a = *reinterpret_cast<const float4*>(xr);
+    x[0] = a.x;
+    x[1] = a.y;
+    x[2] = a.z;
+    x[3] = a.w;
+    if constexpr (TN > 4) {
+      const float4 b = *reinterpret_cast<const float4*>(xr + 4);
+#pragma unroll
+      for (int t = 4; t < TN; ++t) x[t] = (t == 4 ? b.x : t == 5 ? b.y : t == 6 ? b.z : b.w);
+    }
+  } else {
+#pragma unroll
+    for (int t = 0; t < TN; ++t) x[t] = xr[t];
+  }
+}
+
+// Phase A of one warp chunk: lam = W h + eps for `rows` rows x NT frames,
+// q = (v+eps)/lam^2 and r = 1/lam staged into the warp's Q/R rows, optional
+// IS-divergence of each valid cell (online.hpp:303-309) into divacc.
+template <int TK, int TN>
+__device__ __forceinline__ void phase_a(const float* Ws, const float* Hs, float* QR, const float* const* fptr,
+                                        int WS, int c0, int rows, int nf, float eps, bool want_div, int lane,
+                                        float& divacc) {
+  constexpr int KP = 4 * TK, NT = 4 * TN;
+  if (rows == kChunk) {
+    const int rg = lane & 7, fg = lane >> 3;  // 8 row groups x 4 frame groups
+    float vv[4][TN];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        const int n = fg * TN + j;
+        vv[i][j] = n < nf ? __ldg(fptr[n] + c0 + rg + 8 * i) : 0.0f;
+      }
+    float acc[4][TN];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j) acc[i][j] = 0.0f;
+    const float* wrow = Ws + (c0 + rg) * WS;
+    const float* hrow = Hs + fg * TN * KP;
+#pragma unroll
+    for (int kc = 0; kc < KP / 4; ++kc) {
+      float4 w4[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) w4[i] = *reinterpret_cast<const float4*>(wrow + 8 * i * WS + 4 * kc);
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        const float4 h4 = *reinterpret_cast<const float4*>(hrow + j * KP + 4 * kc);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          acc[i][j] = fmaf(w4[i].x, h4.x, acc[i][j]);
+          acc[i][j] = fmaf(w4[i].y, h4.y, acc[i][j]);
+          acc[i][j] = fmaf(w4[i].z, h4.z, acc[i][j]);
+          acc[i][j] = fmaf(w4[i].w, h4.w, acc[i][j]);
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float* qrow = QR + (rg + 8 * i) * kQS + fg * 8;
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        const bool valid = fg * TN + j < nf;
+        const float lam = acc[i][j] + eps;
+        const float r = rcp_approx(lam);
+        const float vpe = vv[i][j] + eps;
+        const float q = vpe * r * r;
+        if (want_div && valid) divacc += is_term_ratio(vpe * r);
+        qrow[j] = valid ? q : 0.0f;
+        qrow[32 + j] = valid ? r : 0.0f;
+      }
+    }
+  } else {
+    // tail rows (F not a multiple of 32 per warp): one (row, frame) cell per lane
+    for (int cell = lane; cell < rows * NT; cell += 32) {
+      const int rl = cell / NT, n = cell - rl * NT;
+      const float* wr = Ws + (c0 + rl) * WS;
+      const float* hr = Hs + n * KP;
+      float acc = 0.0f;
+#pragma unroll
+      for (int kc = 0; kc < KP / 4; ++kc) {
+        const float4 w4 = *reinterpret_cast<const float4*>(wr + 4 * kc);
+        const float4 h4 = *reinterpret_cast<const float4*>(hr + 4 * kc);
+        acc = fmaf(w4.x, h4.x, acc);
+        acc = fmaf(w4.y, h4.y, acc);
+        acc = fmaf(w4.z, h4.z, acc);
+        acc = fmaf(w4.w, h4.w, acc);
+      }
+      const bool valid = n < nf;
+      const float v = valid ? __ldg(fptr[n] + c0 + rl) : 0.0f;
+      const float lam = acc + eps;
+      const float r = rcp_approx(lam);
+      const float vpe = v + eps;
+      const float q = vpe * r * r;
+      if (want_div && valid) divacc += is_term_ratio(vpe * r);
+      float* qrow = QR + rl * kQS + (n / TN) * 8 + (n % TN);
+      qrow[0] = valid ? q : 0.0f;
+      qrow[32] = valid ? r : 0.0f;
+    }
+  }
+}
+
+template <int TK, int TN>
+__global__ void __launch_bounds__(kThreads, 1) solve_kernel(const SolveArgs a) {
+  using S = SolveShape<TK, TN>;
+  using KM = KMap<TK>;
+  constexpr int KP = S::KP, NT = S::NT, PBS = S::PBS;
+  if (*a.status || (a.halt && *a.halt)) return;
+
+  extern __shared__ __align__(16) float smem[];
+  const int WS = a.WS, F = a.F, K = a.K;
+  float* Ws = smem;           // [F][WS]
+  float* Hs = Ws + F * WS;    // [NT][KP]
+  float* UN = Hs + NT * KP;   // union: per-warp Q/R staging | per-lane B partials
+  __shared__ const float* fptr[NT];
+  __shared__ double red[kWarps];
+  __shared__ double meanv[NT];
+  __shared__ int s_bad;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n0 = blockIdx.x * NT;
+  const int nf = min(NT, a.nframes - n0);
+
+  {  // dictionary -> smem (row stride WS, pads are zero in W32)
+    const float4* src = reinterpret_cast<const float4*>(a.W32);
+    float4* dst = reinterpret_cast<float4*>(Ws);
+    const int n4 = F * WS / 4;
+    for (int i = tid; i < n4; i += kThreads) dst[i] = __ldg(src + i);
+  }
+  if (tid < NT) {
+    const int64_t fr = tid < nf ? (a.vsel ? a.vsel[n0 + tid] : a.v0 + n0 + tid) : 0;
+    fptr[tid] = a.V + fr * a.ldv;
+  }
+  if (tid == 0) s_bad = 0;
+  __syncthreads();
+
+  if (a.h0_mode == 2) {  // mean of each frame in fp64 (fresh_h_init's v.mean())
+    for (int n = warp; n < nf; n += kWarps) {
+      double s = 0.0;
+      for (int f = lane; f < F; f += 32) s += double(fptr[n][f]);
+      s = warp_sum_d(s);
+      if (lane == 0) meanv[n] = s / double(F);
+    }
+    __syncthreads();
+  }
+
+  // h0 -> Hs
+  for (int idx = tid; idx < NT * KP; idx += kThreads) {
+    const int n = idx / KP, k = idx - n * KP;
+    float val = 0.0f;
+    if (n < nf && k < K) {
+      if (a.h0_mode == 0) {
+        val = a.H0[size_t(n0 + n) * K + k];
+      } else if (a.h0_mode == 1) {
+        const int64_t col = a.widx ? int64_t(a.widx[n0 + n]) : (a.wbase + n0 + n) % a.wmod;
+        const uint32_t tag = a.T[col];
+        const double ratio = a.P[size_t(a.c_now) * K + k] / a.P[size_t(tag) * K + k];
+        val = float(double(a.U[size_t(col) * K + k]) * ratio);
+      } else {
+        const double mv = meanv[n] > a.epsd ? meanv[n] : a.epsd;
+        val = float(mv / a.kst->kmeanw * a.u01[size_t(n0 + n) * K + k]);
+      }
+      if (a.hscale) val = float(double(val) * a.hscale[k]);
+      if (a.check_h0 && !(val > 0.0f)) s_bad = 1;
+    }
+    Hs[idx] = val;
+  }
+  __syncthreads();
+  if (s_bad) {
+    if (tid == 0) atomicOr(a.status, ST_NONPOS_INIT);
+    return;
+  }
+
+  const int r0 = (warp * F) / kWarps, r1 = ((warp + 1) * F) / kWarps;
+  float* QR = UN + warp * (kChunk * kQS);
+  const float eps = a.eps;
+  float divacc = 0.0f;
+
+  // phase-B lane roles: 4 k groups x 4 frame groups x {num, den}
+  const int kg = lane & 3, ng = (lane >> 2) & 3, nd = lane >> 4;
+
+  for (int pass = 0; pass < a.iters; ++pass) {
+    const bool want_div = a.div_first && pass == 0;
+    float accB[TK][TN];
+#pragma unroll
+    for (int j = 0; j < TK; ++j)
+#pragma unroll
+      for (int t = 0; t < TN; ++t) accB[j][t] = 0.0f;
+
+    for (int c0 = r0; c0 < r1; c0 += kChunk) {
+      const int rows = min(kChunk, r1 - c0);
+      phase_a<TK, TN>(Ws, Hs, QR, fptr, WS, c0, rows, nf, eps, want_div, lane, divacc);
+      __syncwarp();
+      // ---------------- phase B: num += W^T q, den += W^T r (this warp's rows)
+#pragma unroll 2
+      for (int rl = 0; rl < rows; ++rl) {
+        float w[TK];
+        load_wk<TK>(Ws + (c0 + rl) * WS, kg, w);
+        float x[TN];
+        load_x<TN>(QR + rl * kQS + nd * 32 + ng * 8, x);
+#pragma unroll
+        for (int j = 0; j < TK; ++j)
+#pragma unroll
+          for (int t = 0; t < TN; ++t) accB[j][t] = fmaf(w[j], x[t], accB[j][t]);
+      }
+      __syncwarp();
+    }
+
+    // ---------------- cross-warp num/den reduction (fixed order) + MM update
+    __syncthreads();  // every warp is done with its Q/R staging (aliases UN)
+    {
+      float* pb = UN + (warp * 32 + lane) * PBS;
+#pragma unroll
+      for (int j = 0; j < TK; ++j)
+#pragma unroll
+        for (int t = 0; t < TN; ++t) pb[j * TN + t] = accB[j][t];
+    }
+    __syncthreads();
+    for (int p = tid; p < K * nf; p += kThreads) {
+      const int k = p / nf, n = p - k * nf;
+      int kgp, jp;
+      KM::inv(k, kgp, jp);
+      const int ngp = n / TN, tp = n - ngp * TN;
+      const int cell = jp * TN + tp;
+      const int l0 = kgp + 4 * ngp;
+      float num = 0.0f, den = 0.0f;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) {
+        num += UN[(w * 32 + l0) * PBS + cell];
+        den += UN[(w * 32 + l0 + 16) * PBS + cell];
+      }
+      float& h = Hs[n * KP + k];
+      h = h * sqrtf(num / den);
+    }
+    __syncthreads();
+  }
+
+  if (a.do_stats) {
+    const bool want_div = !a.div_first || a.iters == 0;
+    const int rgs = lane & 7, kgs = lane >> 3;
+    for (int c0 = r0; c0 < r1; c0 += kChunk) {
+      const int rows = min(kChunk, r1 - c0);
+      phase_a<TK, TN>(Ws, Hs, QR, fptr, WS, c0, rows, nf, eps, want_div, lane, divacc);
+      __syncwarp();
+      if (!a.stats) continue;
+      // ---------------- statistics: sa[f,k] = sum_n q[f,n] h[k,n], sb with r
+      float sa[4][TK], sb[4][TK];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < TK; ++j) sa[i][j] = sb[i][j] = 0.0f;
+      const int islots = (rows + 7) / 8;
+      for (int n = 0; n < nf; ++n) {
+        float hk[TK];
+        load_wk<TK>(Hs + n * KP, kgs, hk);
+        const int off = (n / TN) * 8 + (n % TN);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (i < islots) {
+            const float q = QR[(rgs + 8 * i) * kQS + off];
+            const float r = QR[(rgs + 8 * i) * kQS + 32 + off];
+#pragma unroll
+            for (int j = 0; j < TK; ++j) {
+              sa[i][j] = fmaf(q, hk[j], sa[i][j]);
+              sb[i][j] = fmaf(r, hk[j], sb[i][j]);
+            }
+          }
+        }
+      }
+      float* outA = a.stats + size_t(blockIdx.x) * 2 * F * KP;
+      float* outB = outA + size_t(F) * KP;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int rl = rgs + 8 * i;
+        if (rl < rows) {
+          const int f = c0 + rl;
+#pragma unroll
+          for (int j = 0; j < TK; ++j) {
+            const int k = KM::k_of(kgs, j);
+            outA[size_t(f) * KP + k] = sa[i][j];
+            outB[size_t(f) * KP + k] = sb[i][j];
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+
+  // divergence partial of this CTA (fixed-order reduction)
+  if (a.divpart) {
+    double d = warp_sum_d(double(divacc));
+    if (lane == 0) red[warp] = d;
+    __syncthreads();
+    if (tid == 0) {
+      double s = 0.0;
+      for (int w = 0; w < kWarps; ++w) s += red[w];
+      a.divpart[blockIdx.x] = s;
+    }
+  }
+
+  // final activations
+  if (a.Hout || a.write_store) {
+    for (int idx = tid; idx < nf * K; idx += kThreads) {
+      const int n = idx / K, k = idx - n * K;
+      const float h = Hs[n * KP + k];
+      if (a.Hout) a.Hout[size_t(n0 + n) * K + k] = h;
+      if (a.write_store) {
+        const int64_t col = a.widx ? int64_t(a.widx[n0 + n]) : (a.wbase + n0 + n) % a.wmod;
+        a.U[size_t(col) * K + k] = h;
+        if (k == 0) a.T[col] = a.c_now;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2 — reduce per-CTA partials into pending; commit part 1.
+// ---------------------------------------------------------------------------
+struct ReduceArgs {
+  const float* stats;
+  const double* divpart;
+  int nblk, F, K, KP;
+  int nframes;
+  const double* W64;  // [F][K]
+  double* pa;         // pending_a [F][K]
+  double* pb;
+  double* A;
+  double* B;
+  double* Wtmp;
+  int do_commit;
+  double rho;
+  DevState* st;
+  const unsigned int* halt;
+};
+
+__global__ void reduce_kernel(const ReduceArgs a) {
+  if (a.st->status || *a.halt) return;
+  const int cell = blockIdx.x * blockDim.x + threadIdx.x;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    double d = 0.0;
+    for (int b = 0; b < a.nblk; ++b) d += a.divpart[b];
+    a.st->pending_div += d;
+    a.st->pending_count += (unsigned long long)a.nframes;
+    a.st->t += (unsigned long long)a.nframes;
+  }
+  if (cell >= a.F * a.K) return;
+  const int f = cell / a.K, k = cell - f * a.K;
+  const size_t off = size_t(f) * a.KP + k;
+  const size_t plane = size_t(a.F) * a.KP;
+  double sa = 0.0, sb = 0.0;
+  for (int b = 0; b < a.nblk; ++b) {
+    const float* p = a.stats + size_t(b) * 2 * plane;
+    sa += double(p[off]);
+    sb += double(p[plane + off]);
+  }
+  const double w = a.W64[cell];
+  const double pa = a.pa[cell] + w * w * sa;
+  const double pb = a.pb[cell] + sb;
+  if (!a.do_commit) {
+    a.pa[cell] = pa;
+    a.pb[cell] = pb;
+    return;
+  }
+  const double An = a.rho * a.A[cell] + pa;  // rho scales the past (online.hpp:319-320)
+  const double Bn = a.rho * a.B[cell] + pb;
+  a.A[cell] = An;
+  a.B[cell] = Bn;
+  a.pa[cell] = 0.0;
+  a.pb[cell] = 0.0;
+  double wn = w;
+  if (Bn > 0.0)
+    wn = sqrt(An / Bn);
+  else if (An > 0.0)
+    atomicOr(&a.st->status, ST_INCONSISTENT);
+  if (!isfinite(wn)) atomicOr(&a.st->status, ST_NONFINITE_W);
+  a.Wtmp[cell] = wn;
+}
+
+// ---------------------------------------------------------------------------
+// K3 — column renormalisation, ||dW||_F, trace point, stop rule.
+// ---------------------------------------------------------------------------
+struct CommitArgs {
+  int F, K, WS;
+  const double* Wtmp;
+  double* W64;
+  double* A;
+  double* B;
+  float* W32;
+  double* P;       // prefix products of the column scales [commits+1][K]
+  double* colpart; // [2][K]
+  DevState* st;
+  unsigned int* halt;
+  double eta;
+  unsigned long long* tr_t;
+  double* tr_obj;
+  unsigned long long* tr_ns;
+  long long tr_cap;
+  double* scale_out;  // optional: column scales s_k of this commit (batch H compensation)
+  int batch_mode;  // 1: no eta halt here (batch stops on the host-visible epoch)
+};
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void commit_kernel(const CommitArgs a) {
+  if (a.st->status || *a.halt) return;
+  const int k = blockIdx.x, tid = threadIdx.x;
+  __shared__ double sh[256];
+  __shared__ double s_scale;
+  double s = 0.0;
+  for (int f = tid; f < a.F; f += blockDim.x) s += a.Wtmp[size_t(f) * a.K + k];
+  sh[tid] = s;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (tid < o) sh[tid] += sh[tid + o];
+    __syncthreads();
+  }
+  if (tid == 0) s_scale = sh[0];
+  __syncthreads();
+  const double sc = s_scale;
+  if (!(sc > 0.0)) {
+    if (tid == 0) atomicOr(&a.st->status, ST_ZERO_COLUMN);
+    return;
+  }
+  double d2 = 0.0, cw = 0.0;
+  for (int f = tid; f < a.F; f += blockDim.x) {
+    const size_t i = size_t(f) * a.K + k;
+    const double wn = a.Wtmp[i] / sc;
+    const double d = wn - a.W64[i];
+    d2 += d * d;
+    cw += wn;
+    a.W64[i] = wn;
+    a.A[i] /= sc;
+    a.B[i] *= sc;
+    a.W32[size_t(f) * a.WS + k] = float(wn);
+  }
+  __syncthreads();
+  sh[tid] = d2;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (tid < o) sh[tid] += sh[tid + o];
+    __syncthreads();
+  }
+  if (tid == 0) a.colpart[k] = sh[0];
+  __syncthreads();
+  sh[tid] = cw;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (tid < o) sh[tid] += sh[tid + o];
+    __syncthreads();
+  }
+  if (tid == 0) {
+    a.colpart[a.K + k] = sh[0];
+    if (a.scale_out) a.scale_out[k] = sc;
+    const unsigned long long c = a.st->commits;
+    a.P[size_t(c + 1) * a.K + k] = a.P[size_t(c) * a.K + k] * sc;
+    __threadfence();
+    const unsigned int ticket = atomicAdd(&a.st->ticket, 1u);
+    if (ticket == unsigned(a.K - 1)) {  // last column done: scalar epilogue
+      __threadfence();
+      double dd = 0.0, ww = 0.0;
+      for (int kk = 0; kk < a.K; ++kk) {
+        dd += ((volatile double*)a.colpart)[kk];
+        ww += ((volatile double*)a.colpart)[a.K + kk];
+      }
+      DevState* st = a.st;
+      st->last_delta = sqrt(dd);
+      st->kmeanw = double(a.K) * (ww / (double(a.F) * double(a.K)));
+      st->last_obj = st->pending_count ? st->pending_div / double(st->pending_count) : 0.0;
+      const long long ti = (long long)(c - st->trace_base);
+      if (a.tr_t && ti >= 0 && ti < a.tr_cap) {
+        a.tr_t[ti] = st->t;
+        a.tr_obj[ti] = st->last_obj;
+        a.tr_ns[ti] = globaltimer_ns();
+      }
+      st->pending_div = 0.0;
+      st->pending_count = 0;
+      st->commits = c + 1;
+      st->ticket = 0;
+      if (!a.batch_mode && a.eta > 0.0 && st->last_delta < a.eta) *a.halt = 1u;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K0 — std::mt19937_64 (libstdc++ algorithm) per frame for fresh restarts.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t splitmix64_d(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+
+__global__ void fresh_kernel(uint64_t seed, uint64_t t0, int n, int K, double* u01) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  constexpr int NN = 312, MM = 156;
+  constexpr uint64_t UM = 0xFFFFFFFF80000000ULL, LM = 0x7FFFFFFFULL, MA = 0xB5026F5AA96619E9ULL;
+  uint64_t mt[NN];
+  // make_engine(mix_seed(seed, t)) = mt19937_64(splitmix64(mix_seed(seed, t)))  (rng.hpp:17-23)
+  const uint64_t ms = splitmix64_d(splitmix64_d(seed) ^ splitmix64_d(~(t0 + uint64_t(i))));
+  mt[0] = splitmix64_d(ms);
+  for (int j = 1; j < NN; ++j) mt[j] = 6364136223846793005ULL * (mt[j - 1] ^ (mt[j - 1] >> 62)) + uint64_t(j);
+  int p = NN;
+  for (int k = 0; k < K; ++k) {
+    if (p >= NN) {
+      int j = 0;
+      for (; j < NN - MM; ++j) {
+        const uint64_t y = (mt[j] & UM) | (mt[j + 1] & LM);
+        mt[j] = mt[j + MM] ^ (y >> 1) ^ ((y & 1ULL) ? MA : 0ULL);
+      }
+      for (; j < NN - 1; ++j) {
+        const uint64_t y = (mt[j] & UM) | (mt[j + 1] & LM);
+        mt[j] = mt[j + (MM - NN)] ^ (y >> 1) ^ ((y & 1ULL) ? MA : 0ULL);
+      }
+      const uint64_t y = (mt[NN - 1] & UM) | (mt[0] & LM);
+      mt[NN - 1] = mt[MM - 1] ^ (y >> 1) ^ ((y & 1ULL) ? MA : 0ULL);
+      p = 0;
+    }
+    uint64_t z = mt[p++];
+    z ^= (z >> 29) & 0x5555555555555555ULL;
+    z ^= (z << 17) & 0x71D67FFFEDA60000ULL;
+    z ^= (z << 37) & 0xFFF7EEE000000000ULL;
+    z ^= (z >> 43);
+    u01[size_t(i) * K + k] = 1.0 - double(z >> 11) * 0x1.0p-53;  // uniform_open01 (rng.hpp:27-34)
+  }
+}
+
+}  // namespace isnmf_dev
