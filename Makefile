@@ -19,3 +19,9 @@ oracle:
 clean:
 	rm -rf $(PKG)/lib oracle/_build
 .PHONY: all oracle clean
+
+# experimental build with per-phase cycle counters (K1 headline variant only)
+prof: $(SRC) $(DEPS)
+	@mkdir -p $(PKG)/lib_prof
+	$(NVCC) $(NVFLAGS) -DISNMF_PHASE_PROF -DISNMF_MIN_VARIANTS -shared -o $(PKG)/lib_prof/libisnmf_b200.so $(SRC) -lcudart 2> $(PKG)/lib_prof/ptxas.log || (cat $(PKG)/lib_prof/ptxas.log; exit 1)
+.PHONY: prof

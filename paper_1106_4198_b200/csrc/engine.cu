@@ -61,12 +61,15 @@ using SolveFn = void (*)(const SolveArgs);
 struct Variant {
   int TK, TN;
   SolveFn fn;
-  size_t (*smem)(int, int);
+  size_t (*smem)(int);
   size_t static_smem;
   bool configured;
 };
 
 #define VAR(tk, tn) {tk, tn, solve_kernel<tk, tn>, &SolveShape<tk, tn>::smem_bytes, 0, false}
+#ifdef ISNMF_MIN_VARIANTS  // fast experimental builds: the headline shape only
+Variant g_variants[] = {VAR(13, 7), VAR(5, 2), VAR(3, 1)};
+#else
 Variant g_variants[] = {
     VAR(1, 1), VAR(1, 2), VAR(1, 4), VAR(1, 7), VAR(1, 8),       //
     VAR(2, 1), VAR(2, 2), VAR(2, 4), VAR(2, 7), VAR(2, 8),       //
@@ -76,6 +79,7 @@ Variant g_variants[] = {
     VAR(13, 1), VAR(13, 2), VAR(13, 4), VAR(13, 7), VAR(13, 8),  //
     VAR(16, 1), VAR(16, 2), VAR(16, 4), VAR(16, 7),              //
 };
+#endif
 #undef VAR
 constexpr int kNumVariants = sizeof(g_variants) / sizeof(g_variants[0]);
 
@@ -128,7 +132,7 @@ int pick_variant(int64_t F, int64_t K, int64_t frames, Variant** out, int* WS, s
                             smem_optin() - int(best->static_smem)));
     best->configured = true;
   }
-  const size_t sm = best->smem(int(F), w);
+  const size_t sm = best->smem(int(F));
   if (sm + best->static_smem > size_t(smem_optin()))
     return fail(ISNMF_E_UNSUPPORTED, "F=%lld, K=%lld: dictionary (%zu B) does not fit shared memory", (long long)F,
                 (long long)K, sm);
@@ -148,16 +152,6 @@ int dalloc(T** p, size_t n) {
 
 void dfree(void* p) {
   if (p) cudaFree(p);
-}
-
-// col-major F x K (host, fp64) <-> row-major [F][K]
-void to_rowmajor(const double* cm, int64_t F, int64_t K, double* rm) {
-  for (int64_t k = 0; k < K; ++k)
-    for (int64_t f = 0; f < F; ++f) rm[f * K + k] = cm[k * F + f];
-}
-void to_colmajor(const double* rm, int64_t F, int64_t K, double* cm) {
-  for (int64_t k = 0; k < K; ++k)
-    for (int64_t f = 0; f < F; ++f) cm[k * F + f] = rm[f * K + k];
 }
 
 bool is_device_ptr(const void* p) {
@@ -256,6 +250,7 @@ struct isnmf_online {
   size_t ev_used = 0;
   int64_t prof_frames = 0;
   cudaEvent_t ev_span[2] = {nullptr, nullptr};
+  long long* phase_prof = nullptr;  // ISNMF_PHASE_PROF builds only
 };
 
 namespace {
@@ -335,7 +330,6 @@ int launch_block(isnmf_online* c, const float* dv, int64_t ldv, int nb, const ui
   a.W32 = c->W32;
   a.F = c->F;
   a.K = c->K;
-  a.WS = c->WS;
   a.V = dv;
   a.ldv = ldv;
   a.vsel = nullptr;
@@ -363,6 +357,7 @@ int launch_block(isnmf_online* c, const float* dv, int64_t ldv, int nb, const ui
   a.divpart = c->divpart;
   a.status = &c->st->status;
   a.halt = &c->st->halt;
+  a.prof = c->phase_prof;
   if (c->prof) {
     while (c->ev_pool.size() < c->ev_used + 2) {
       cudaEvent_t e;
@@ -396,7 +391,7 @@ int launch_block(isnmf_online* c, const float* dv, int64_t ldv, int nb, const ui
   r.rho = c->rho;
   r.st = c->st;
   r.halt = &c->st->halt;
-  reduce_kernel<<<(c->F * c->K + 255) / 256, 256, 0, c->cs>>>(r);
+  reduce_kernel<<<(c->F * c->K + 127) / 128, 256, 0, c->cs>>>(r);
   c->launches += 2;
   if (commit) {
     CommitArgs m{};
@@ -585,7 +580,7 @@ int isnmf_online_create(isnmf_online** out, const isnmf_online_config* cfg) {
       (rc = dalloc(&c->B, FK)) || (rc = dalloc(&c->pa, FK)) || (rc = dalloc(&c->pb, FK)) ||
       (rc = dalloc(&c->Wtmp, FK)) || (rc = dalloc(&c->colpart, 2 * size_t(c->K))) ||
       (rc = dalloc(&c->W32, size_t(c->F) * c->WS)) ||
-      (rc = dalloc(&c->stats, size_t(c->maxblk) * 2 * c->F * c->KP)) || (rc = dalloc(&c->divpart, c->maxblk)) ||
+      (rc = dalloc(&c->stats, size_t(c->maxblk) * 2 * c->F * c->KP + 4)) || (rc = dalloc(&c->divpart, c->maxblk)) ||
       (rc = dalloc(&c->Hlast, size_t(c->beta) * c->K)))
     return bail(rc);
   if (c->restart == ISNMF_RESTART_FRESH && (rc = dalloc(&c->u01, size_t(c->beta) * c->K))) return bail(rc);
@@ -622,8 +617,7 @@ int isnmf_online_set_dictionary(isnmf_online* c, const double* w, const double* 
   std::vector<double> rm(size_t(F * K));
   CU(cudaStreamSynchronize(c->cs));
   if (w) {
-    to_rowmajor(w, F, K, rm.data());
-    CU(cudaMemcpy(c->W64, rm.data(), rm.size() * sizeof(double), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(c->W64, w, rm.size() * sizeof(double), cudaMemcpyHostToDevice));
     std::vector<float> w32(size_t(F) * c->WS, 0.0f);
     double sum = 0.0;
     for (int64_t k = 0; k < K; ++k)
@@ -636,14 +630,8 @@ int isnmf_online_set_dictionary(isnmf_online* c, const double* w, const double* 
     CU(cudaMemcpy(reinterpret_cast<char*>(c->st) + offsetof(DevState, kmeanw), &kmeanw, sizeof(double),
                   cudaMemcpyHostToDevice));
   }
-  if (a) {
-    to_rowmajor(a, F, K, rm.data());
-    CU(cudaMemcpy(c->A, rm.data(), rm.size() * sizeof(double), cudaMemcpyHostToDevice));
-  }
-  if (b) {
-    to_rowmajor(b, F, K, rm.data());
-    CU(cudaMemcpy(c->B, rm.data(), rm.size() * sizeof(double), cudaMemcpyHostToDevice));
-  }
+  if (a) CU(cudaMemcpy(c->A, a, rm.size() * sizeof(double), cudaMemcpyHostToDevice));
+  if (b) CU(cudaMemcpy(c->B, b, rm.size() * sizeof(double), cudaMemcpyHostToDevice));
   return 0;
 }
 
@@ -655,10 +643,7 @@ int isnmf_online_get_dictionary(isnmf_online* c, double* w, double* a, double* b
   double* src[3] = {c->W64, c->A, c->B};
   double* dst[3] = {w, a, b};
   for (int i = 0; i < 3; ++i)
-    if (dst[i]) {
-      CU(cudaMemcpy(rm.data(), src[i], rm.size() * sizeof(double), cudaMemcpyDeviceToHost));
-      to_colmajor(rm.data(), F, K, dst[i]);
-    }
+    if (dst[i]) CU(cudaMemcpy(dst[i], src[i], rm.size() * sizeof(double), cudaMemcpyDeviceToHost));
   return 0;
 }
 
@@ -668,14 +653,8 @@ int isnmf_online_set_pending(isnmf_online* c, const double* pa, const double* pb
   const int64_t F = c->F, K = c->K;
   std::vector<double> rm(size_t(F * K));
   CU(cudaStreamSynchronize(c->cs));
-  if (pa) {
-    to_rowmajor(pa, F, K, rm.data());
-    CU(cudaMemcpy(c->pa, rm.data(), rm.size() * sizeof(double), cudaMemcpyHostToDevice));
-  }
-  if (pb) {
-    to_rowmajor(pb, F, K, rm.data());
-    CU(cudaMemcpy(c->pb, rm.data(), rm.size() * sizeof(double), cudaMemcpyHostToDevice));
-  }
+  if (pa) CU(cudaMemcpy(c->pa, pa, rm.size() * sizeof(double), cudaMemcpyHostToDevice));
+  if (pb) CU(cudaMemcpy(c->pb, pb, rm.size() * sizeof(double), cudaMemcpyHostToDevice));
   DevState h;
   CU(cudaMemcpy(&h, c->st, sizeof(h), cudaMemcpyDeviceToHost));
   h.pending_div = pending_div;
@@ -689,14 +668,8 @@ int isnmf_online_get_pending(isnmf_online* c, double* pa, double* pb, double* pe
   const int64_t F = c->F, K = c->K;
   std::vector<double> rm(size_t(F * K));
   CU(cudaStreamSynchronize(c->cs));
-  if (pa) {
-    CU(cudaMemcpy(rm.data(), c->pa, rm.size() * sizeof(double), cudaMemcpyDeviceToHost));
-    to_colmajor(rm.data(), F, K, pa);
-  }
-  if (pb) {
-    CU(cudaMemcpy(rm.data(), c->pb, rm.size() * sizeof(double), cudaMemcpyDeviceToHost));
-    to_colmajor(rm.data(), F, K, pb);
-  }
+  if (pa) CU(cudaMemcpy(pa, c->pa, rm.size() * sizeof(double), cudaMemcpyDeviceToHost));
+  if (pb) CU(cudaMemcpy(pb, c->pb, rm.size() * sizeof(double), cudaMemcpyDeviceToHost));
   DevState h;
   CU(cudaMemcpy(&h, c->st, sizeof(h), cudaMemcpyDeviceToHost));
   if (pending_div) *pending_div = h.pending_div;
@@ -849,6 +822,22 @@ int isnmf_online_get_last_h(isnmf_online* c, double* h, int64_t n) {
 
 int64_t isnmf_online_launch_count(isnmf_online* c) { return c ? c->launches : -1; }
 
+#ifdef ISNMF_PHASE_PROF
+// Debug hook of ISNMF_PHASE_PROF builds: per-(CTA, warp) cycles per K1 phase.
+int isnmf_debug_phase_prof(isnmf_online* c, long long* out, int64_t cap, int32_t reset) {
+  const size_t n = size_t(c->maxblk) * kWarps * 8;
+  if (!c->phase_prof) {
+    CU(cudaMalloc(&c->phase_prof, n * sizeof(long long)));
+    CU(cudaMemset(c->phase_prof, 0, n * sizeof(long long)));
+  }
+  CU(cudaStreamSynchronize(c->cs));
+  if (out) CU(cudaMemcpy(out, c->phase_prof, std::min<size_t>(n, size_t(cap)) * sizeof(long long),
+                         cudaMemcpyDeviceToHost));
+  if (reset) CU(cudaMemset(c->phase_prof, 0, n * sizeof(long long)));
+  return 0;
+}
+#endif
+
 int isnmf_online_profile_begin(isnmf_online* c) {
   if (!c) return fail(ISNMF_E_INVALID_ARG, "NULL context");
   for (int i = 0; i < 2; ++i)
@@ -983,7 +972,7 @@ struct SolveWork {
     TRY(dalloc(&colpart, 2 * size_t(K)));
     TRY(dalloc(&P, 2 * size_t(K)));
     TRY(dalloc(&scale, size_t(K)));
-    TRY(dalloc(&stats, size_t(seg_blocks) * 2 * F * KP));
+    TRY(dalloc(&stats, size_t(seg_blocks) * 2 * F * KP + 4));
     TRY(dalloc(&divpart, size_t(seg_blocks)));
     TRY(dalloc(&halt, 1));
     CU(cudaMemset(halt, 0, sizeof(unsigned int)));
@@ -999,9 +988,7 @@ struct SolveWork {
 
   // W from host column-major fp64 (F x K)
   int set_w(const double* w) {
-    std::vector<double> rm(size_t(F) * K);
-    to_rowmajor(w, F, K, rm.data());
-    CU(cudaMemcpy(W64, rm.data(), rm.size() * sizeof(double), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(W64, w, size_t(F) * K * sizeof(double), cudaMemcpyHostToDevice));
     std::vector<float> w32(size_t(F) * WS, 0.0f);
     for (int64_t k = 0; k < K; ++k)
       for (int64_t f = 0; f < F; ++f) w32[f * WS + k] = float(w[k * F + f]);
@@ -1021,7 +1008,6 @@ struct SolveWork {
       a.W32 = W32;
       a.F = F;
       a.K = K;
-      a.WS = WS;
       a.V = V;
       a.ldv = ldv;
       a.v0 = s0;
@@ -1062,7 +1048,7 @@ struct SolveWork {
       // divergence partials are always folded (reduce_kernel block 0 sums divpart[0..nblk_div))
       r.nblk = nblk;
       if (!stats_on) r.F = 0;
-      reduce_kernel<<<std::max(1, (r.F * K + 255) / 256), 256, 0, s>>>(r);
+      reduce_kernel<<<std::max(1, (r.F * K + 127) / 128), 256, 0, s>>>(r);
       CU(cudaGetLastError());
     }
     return 0;
@@ -1146,15 +1132,8 @@ static int stateless(const double* v, const double* w, const double* h, int64_t 
     for (size_t i = 0; i < h32.size(); ++i) h_out[i] = h32[i];
   }
   if (a_out || b_out) {
-    std::vector<double> rm(size_t(F) * K);
-    if (a_out) {
-      CU(cudaMemcpy(rm.data(), wk.pa, rm.size() * sizeof(double), cudaMemcpyDeviceToHost));
-      to_colmajor(rm.data(), F, K, a_out);
-    }
-    if (b_out) {
-      CU(cudaMemcpy(rm.data(), wk.pb, rm.size() * sizeof(double), cudaMemcpyDeviceToHost));
-      to_colmajor(rm.data(), F, K, b_out);
-    }
+    if (a_out) CU(cudaMemcpy(a_out, wk.pa, size_t(F) * K * sizeof(double), cudaMemcpyDeviceToHost));
+    if (b_out) CU(cudaMemcpy(b_out, wk.pb, size_t(F) * K * sizeof(double), cudaMemcpyDeviceToHost));
   }
   if (div_out) *div_out = st.pending_div;
   return 0;
@@ -1317,7 +1296,7 @@ int isnmf_batch_train(const float* v, int64_t ldv, int64_t F, int64_t N, int64_t
     r.rho = 0.0;
     r.st = wk.st;
     r.halt = wk.halt;
-    reduce_kernel<<<int((F * K + 255) / 256), 256, 0, wk.s>>>(r);
+    reduce_kernel<<<int((F * K + 127) / 128), 256, 0, wk.s>>>(r);
     CommitArgs m{};
     m.F = int(F);
     m.K = int(K);
@@ -1376,9 +1355,7 @@ int isnmf_batch_train(const float* v, int64_t ldv, int64_t F, int64_t N, int64_t
       *initial_obj = obj;
     }
   }
-  std::vector<double> rm(size_t(F) * K);
-  CU(cudaMemcpy(rm.data(), wk.W64, rm.size() * sizeof(double), cudaMemcpyDeviceToHost));
-  to_colmajor(rm.data(), F, K, w_out);
+  CU(cudaMemcpy(w_out, wk.W64, size_t(F) * K * sizeof(double), cudaMemcpyDeviceToHost));
   std::vector<float> h32(size_t(K) * N);
   CU(cudaMemcpy(h32.data(), dh, h32.size() * sizeof(float), cudaMemcpyDeviceToHost));
   for (size_t i = 0; i < h32.size(); ++i) h_out[i] = h32[i];

@@ -14,9 +14,10 @@
 //                      with splitmix64(mix_seed(seed, t)) (online.hpp:294-301,
 //                      rng.hpp:10-34), bit-exact.
 //
-// Layout in HBM (row-major [F][K] for the fp64 state so the reduce kernel is
-// coalesced; W32 is the solver's fp32 copy with row stride WS >= K padded with
-// zero columns).  See DESIGN.md for the roofline of each kernel.
+// Layout in HBM: the fp64 state (W, A, B, pending, Wtmp) is column-major
+// F x K like the reference's Eigen matrices (coalesced per-column commit);
+// per-CTA statistics partials are [2][KP][F] planes at the same cell offsets;
+// W32 is the solver's fp32 copy, row-major [F][WS] with zero pad columns.  See DESIGN.md for the roofline of each kernel.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -28,7 +29,9 @@ namespace isnmf_dev {
 constexpr int kWarps = 8;
 constexpr int kThreads = kWarps * 32;
 constexpr int kChunk = 32;  // rows of F per warp chunk
-constexpr int kQS = 68;     // floats per Q/R staging row: [nd 2][ng 4][8] + 4 skew
+constexpr int kQS = 68;     // floats per Q/R staging row: q at [ng 4][8], r at 36 + [ng 4][8]
+constexpr int kQR_R = 36;   // r half offset: 32 + 4 skew so the 8 (nd, ng) float4 reads of phase B
+                            // hit 8 distinct 16-byte bank groups
 
 enum : uint32_t {
   ST_NONPOS_INIT = 1u,
@@ -56,6 +59,21 @@ struct DevState {
   unsigned int pad;
 };
 
+// Optional per-phase cycle instrumentation (build with -DISNMF_PHASE_PROF):
+// per warp, cycles spent in each phase are added to a.prof[(block*8+warp)*8 + phase].
+#ifdef ISNMF_PHASE_PROF
+#define PROF_T0() long long prof_t = clock64()
+#define PROF_MARK(ph)                                                                   \
+  do {                                                                                  \
+    const long long prof_n = clock64();                                                 \
+    if (lane == 0 && a.prof) a.prof[(blockIdx.x * kWarps + warp) * 8 + (ph)] += prof_n - prof_t; \
+    prof_t = prof_n;                                                                    \
+  } while (0)
+#else
+#define PROF_T0()
+#define PROF_MARK(ph)
+#endif
+
 __device__ __forceinline__ float rcp_approx(float x) {
   float r;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
@@ -68,21 +86,20 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // full relative accuracy instead of rounding u to -1.  Relative error <~1e-6.
 __device__ __forceinline__ float is_term_ratio(float ratio) {
   const float u = ratio - 1.0f;
-  if (fabsf(u) < 0.25f) {
-    float p = -1.0f / 12.0f;
-    p = fmaf(p, u, 1.0f / 11.0f);
-    p = fmaf(p, u, -1.0f / 10.0f);
-    p = fmaf(p, u, 1.0f / 9.0f);
-    p = fmaf(p, u, -1.0f / 8.0f);
-    p = fmaf(p, u, 1.0f / 7.0f);
-    p = fmaf(p, u, -1.0f / 6.0f);
-    p = fmaf(p, u, 1.0f / 5.0f);
-    p = fmaf(p, u, -1.0f / 4.0f);
-    p = fmaf(p, u, 1.0f / 3.0f);
-    p = fmaf(p, u, -1.0f / 2.0f);
-    return -(u * u) * p;
-  }
-  const float t = u - logf(ratio);
+  float p = -1.0f / 12.0f;
+  p = fmaf(p, u, 1.0f / 11.0f);
+  p = fmaf(p, u, -1.0f / 10.0f);
+  p = fmaf(p, u, 1.0f / 9.0f);
+  p = fmaf(p, u, -1.0f / 8.0f);
+  p = fmaf(p, u, 1.0f / 7.0f);
+  p = fmaf(p, u, -1.0f / 6.0f);
+  p = fmaf(p, u, 1.0f / 5.0f);
+  p = fmaf(p, u, -1.0f / 4.0f);
+  p = fmaf(p, u, 1.0f / 3.0f);
+  p = fmaf(p, u, -1.0f / 2.0f);
+  const float series = -(u * u) * p;
+  const float direct = u - __logf(ratio);
+  const float t = fabsf(u) < 0.25f ? series : direct;
   return t > 0.0f ? t : 0.0f;
 }
 
@@ -101,8 +118,8 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 // K1 — fused solve.
 // ---------------------------------------------------------------------------
 struct SolveArgs {
-  const float* W32;  // [F][WS]
-  int F, K, WS;
+  const float* W32;  // [F][SolveShape::WS], pad columns zero
+  int F, K;
   const float* V;  // frames; block-local frame n is V + frame(n) * ldv
   int64_t ldv;
   const int64_t* vsel;  // frame(n) = vsel[n] (nullable)
@@ -128,10 +145,11 @@ struct SolveArgs {
   int do_stats;   // extra pass with the final h: divergence (+ statistics when stats != nullptr)
   int div_first;  // divergence from pass 0 (the incoming h) instead of the final pass
   int check_h0;   // flag h0 <= 0 as NonPositiveInit (solve_h, kernels.hpp:67)
-  float* stats;     // [gridDim][2][F][KP]
+  float* stats;     // [gridDim][2][KP][F]
   double* divpart;  // [gridDim]
   unsigned int* status;
   const unsigned int* halt;
+  long long* prof;  // phase cycle counters (ISNMF_PHASE_PROF builds only)
 };
 
 template <int TK>
@@ -158,12 +176,15 @@ template <int TK, int TN>
 struct SolveShape {
   static constexpr int KP = 4 * TK;
   static constexpr int NT = 4 * TN;
+  // dictionary row stride in smem: an odd number of float4s, so the 8 rows a
+  // quarter-warp reads in phase A hit 8 distinct 16-byte bank groups
+  static constexpr int WS = ((KP / 4) % 2 == 1) ? KP : KP + 4;
   static constexpr int cells = TK * TN;
-  static constexpr int pbs0 = (cells + 3) / 4 * 4;
-  static constexpr int PBS = ((pbs0 / 4) % 2 == 0) ? pbs0 + 4 : pbs0;  // 16B-aligned, odd # of float4s
+  // per-lane num/den partial stride: odd, so scalar stores of 32 lanes are conflict-free
+  static constexpr int PBS = (cells % 2 == 1) ? cells : cells + 1;
   static constexpr int union_floats =
       (kWarps * kChunk * kQS > kWarps * 32 * PBS) ? kWarps * kChunk * kQS : kWarps * 32 * PBS;
-  static size_t smem_bytes(int F, int WS) { return sizeof(float) * (size_t(F) * WS + NT * KP + union_floats); }
+  static size_t smem_bytes(int F) { return sizeof(float) * (size_t(F) * WS + NT * KP + union_floats); }
 };
 
 // Loads the lane's TK dictionary values of one row (k-set of group kg).
@@ -201,24 +222,30 @@ __device__ __forceinline__ void load_x(const float* xr, float (&x)[TN]) {
   }
 }
 
-// Phase A of one warp chunk: lam = W h + eps for `rows` rows x NT frames,
-// q = (v+eps)/lam^2 and r = 1/lam staged into the warp's Q/R rows, optional
-// IS-divergence of each valid cell (online.hpp:303-309) into divacc.
+// Phase A of one warp chunk: lam = W h + eps for `rows` rows x NT frames;
+// q = (v+eps)/lam^2 and r = 1/lam are staged into the warp's Q/R rows
+// ([row][nd][ng][8], padding lanes of invalid frames hold 0).
+// V values of a full chunk for this lane's phase-A cells (rows rg+8i, frames
+// fg*TN+j), issued one chunk ahead so the L2 latency hides behind phase B.
+template <int TN>
+__device__ __forceinline__ void load_v(float (&vv)[4][TN], const float* const* fptr, int c0, int nf, int lane) {
+  const int rg = lane & 7, fg = lane >> 3;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      const int n = fg * TN + j;
+      vv[i][j] = n < nf ? __ldg(fptr[n] + c0 + rg + 8 * i) : 0.0f;
+    }
+}
+
 template <int TK, int TN>
 __device__ __forceinline__ void phase_a(const float* Ws, const float* Hs, float* QR, const float* const* fptr,
-                                        int WS, int c0, int rows, int nf, float eps, bool want_div, int lane,
-                                        float& divacc) {
-  constexpr int KP = 4 * TK, NT = 4 * TN;
+                                        int c0, int rows, int nf, float eps, int lane, const float (&vv)[4][TN]) {
+  using S = SolveShape<TK, TN>;
+  constexpr int KP = S::KP, NT = S::NT, WS = S::WS;
   if (rows == kChunk) {
     const int rg = lane & 7, fg = lane >> 3;  // 8 row groups x 4 frame groups
-    float vv[4][TN];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < TN; ++j) {
-        const int n = fg * TN + j;
-        vv[i][j] = n < nf ? __ldg(fptr[n] + c0 + rg + 8 * i) : 0.0f;
-      }
     float acc[4][TN];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
@@ -226,7 +253,7 @@ __device__ __forceinline__ void phase_a(const float* Ws, const float* Hs, float*
       for (int j = 0; j < TN; ++j) acc[i][j] = 0.0f;
     const float* wrow = Ws + (c0 + rg) * WS;
     const float* hrow = Hs + fg * TN * KP;
-#pragma unroll
+#pragma unroll 1
     for (int kc = 0; kc < KP / 4; ++kc) {
       float4 w4[4];
 #pragma unroll
@@ -249,13 +276,10 @@ __device__ __forceinline__ void phase_a(const float* Ws, const float* Hs, float*
 #pragma unroll
       for (int j = 0; j < TN; ++j) {
         const bool valid = fg * TN + j < nf;
-        const float lam = acc[i][j] + eps;
-        const float r = rcp_approx(lam);
-        const float vpe = vv[i][j] + eps;
-        const float q = vpe * r * r;
-        if (want_div && valid) divacc += is_term_ratio(vpe * r);
+        const float r = rcp_approx(acc[i][j] + eps);
+        const float q = (vv[i][j] + eps) * r * r;
         qrow[j] = valid ? q : 0.0f;
-        qrow[32 + j] = valid ? r : 0.0f;
+        qrow[kQR_R + j] = valid ? r : 0.0f;
       }
     }
   } else {
@@ -265,7 +289,7 @@ __device__ __forceinline__ void phase_a(const float* Ws, const float* Hs, float*
       const float* wr = Ws + (c0 + rl) * WS;
       const float* hr = Hs + n * KP;
       float acc = 0.0f;
-#pragma unroll
+#pragma unroll 1
       for (int kc = 0; kc < KP / 4; ++kc) {
         const float4 w4 = *reinterpret_cast<const float4*>(wr + 4 * kc);
         const float4 h4 = *reinterpret_cast<const float4*>(hr + 4 * kc);
@@ -276,30 +300,45 @@ __device__ __forceinline__ void phase_a(const float* Ws, const float* Hs, float*
       }
       const bool valid = n < nf;
       const float v = valid ? __ldg(fptr[n] + c0 + rl) : 0.0f;
-      const float lam = acc + eps;
-      const float r = rcp_approx(lam);
-      const float vpe = v + eps;
-      const float q = vpe * r * r;
-      if (want_div && valid) divacc += is_term_ratio(vpe * r);
+      const float r = rcp_approx(acc + eps);
+      const float q = (v + eps) * r * r;
       float* qrow = QR + rl * kQS + (n / TN) * 8 + (n % TN);
       qrow[0] = valid ? q : 0.0f;
-      qrow[32] = valid ? r : 0.0f;
+      qrow[kQR_R] = valid ? r : 0.0f;
     }
   }
+}
+
+// IS divergence of the staged chunk (online.hpp:303-309 / kernels.hpp:52-53):
+// 1 + u = (v+eps)/lam = q / r, branch-free, four independent partial sums.
+template <int TN>
+__device__ __forceinline__ float chunk_divergence(const float* QR, int rows, int nf, int lane) {
+  constexpr int NT = 4 * TN;
+  float s[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+  const int cells = rows * NT;
+#pragma unroll 4
+  for (int cell = lane; cell < cells; cell += 32) {
+    const int rl = cell / NT, n = cell - rl * NT;
+    const float* qp = QR + rl * kQS + (n / TN) * 8 + (n % TN);
+    const float q = qp[0], r = qp[kQR_R];
+    const float t = (n < nf) ? is_term_ratio(q * rcp_approx(r)) : 0.0f;
+    s[(cell >> 5) & 3] += t;
+  }
+  return (s[0] + s[1]) + (s[2] + s[3]);
 }
 
 template <int TK, int TN>
 __global__ void __launch_bounds__(kThreads, 1) solve_kernel(const SolveArgs a) {
   using S = SolveShape<TK, TN>;
   using KM = KMap<TK>;
-  constexpr int KP = S::KP, NT = S::NT, PBS = S::PBS;
+  constexpr int KP = S::KP, NT = S::NT, PBS = S::PBS, WS = S::WS;
   if (*a.status || (a.halt && *a.halt)) return;
 
   extern __shared__ __align__(16) float smem[];
-  const int WS = a.WS, F = a.F, K = a.K;
+  const int F = a.F, K = a.K;
   float* Ws = smem;           // [F][WS]
   float* Hs = Ws + F * WS;    // [NT][KP]
-  float* UN = Hs + NT * KP;   // union: per-warp Q/R staging | per-lane B partials
+  float* UN = Hs + NT * KP;   // union: per-warp Q/R staging | per-lane num/den partials
   __shared__ const float* fptr[NT];
   __shared__ double red[kWarps];
   __shared__ double meanv[NT];
@@ -308,6 +347,7 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(const SolveArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n0 = blockIdx.x * NT;
   const int nf = min(NT, a.nframes - n0);
+  PROF_T0();
 
   {  // dictionary -> smem (row stride WS, pads are zero in W32)
     const float4* src = reinterpret_cast<const float4*>(a.W32);
@@ -359,16 +399,20 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(const SolveArgs a) {
     return;
   }
 
+  PROF_MARK(0);  // prologue: W -> smem, h0
   const int r0 = (warp * F) / kWarps, r1 = ((warp + 1) * F) / kWarps;
+  // full 32-row chunks of this warp, visited cyclically; V is prefetched one ahead
+  const int nfull = (r1 - r0) / kChunk;
+  auto next_full = [&](int c0) { return (c0 + kChunk < r0 + nfull * kChunk) ? c0 + kChunk : r0; };
+  float vv[4][TN];
+  if (nfull > 0) load_v<TN>(vv, fptr, r0, nf, lane);
   float* QR = UN + warp * (kChunk * kQS);
   const float eps = a.eps;
   float divacc = 0.0f;
-
   // phase-B lane roles: 4 k groups x 4 frame groups x {num, den}
   const int kg = lane & 3, ng = (lane >> 2) & 3, nd = lane >> 4;
 
   for (int pass = 0; pass < a.iters; ++pass) {
-    const bool want_div = a.div_first && pass == 0;
     float accB[TK][TN];
 #pragma unroll
     for (int j = 0; j < TK; ++j)
@@ -377,25 +421,40 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(const SolveArgs a) {
 
     for (int c0 = r0; c0 < r1; c0 += kChunk) {
       const int rows = min(kChunk, r1 - c0);
-      phase_a<TK, TN>(Ws, Hs, QR, fptr, WS, c0, rows, nf, eps, want_div, lane, divacc);
+      phase_a<TK, TN>(Ws, Hs, QR, fptr, c0, rows, nf, eps, lane, vv);
+      if (rows == kChunk) load_v<TN>(vv, fptr, next_full(c0), nf, lane);
       __syncwarp();
-      // ---------------- phase B: num += W^T q, den += W^T r (this warp's rows)
+      if (a.div_first && pass == 0) divacc += chunk_divergence<TN>(QR, rows, nf, lane);
+      PROF_MARK(1);  // phase A
+      // ---------------- phase B: num += W^T q, den += W^T r (this warp's rows),
+      // loads of row rl+1 issued before the FMAs of row rl
+      const float* wr = Ws + c0 * WS;
+      const float* xr = QR + nd * kQR_R + ng * 8;
+      float w[TK], x[TN];
+      load_wk<TK>(wr, kg, w);
+      load_x<TN>(xr, x);
 #pragma unroll 2
       for (int rl = 0; rl < rows; ++rl) {
-        float w[TK];
-        load_wk<TK>(Ws + (c0 + rl) * WS, kg, w);
-        float x[TN];
-        load_x<TN>(QR + rl * kQS + nd * 32 + ng * 8, x);
+        float wn[TK], xn[TN];
+        const int rn = rl + 1 < rows ? rl + 1 : rl;
+        load_wk<TK>(wr + rn * WS, kg, wn);
+        load_x<TN>(xr + rn * kQS, xn);
 #pragma unroll
         for (int j = 0; j < TK; ++j)
 #pragma unroll
           for (int t = 0; t < TN; ++t) accB[j][t] = fmaf(w[j], x[t], accB[j][t]);
+#pragma unroll
+        for (int j = 0; j < TK; ++j) w[j] = wn[j];
+#pragma unroll
+        for (int t = 0; t < TN; ++t) x[t] = xn[t];
       }
       __syncwarp();
+      PROF_MARK(2);  // phase B
     }
 
     // ---------------- cross-warp num/den reduction (fixed order) + MM update
     __syncthreads();  // every warp is done with its Q/R staging (aliases UN)
+    PROF_MARK(3);  // wait at the end-of-pass barrier
     {
       float* pb = UN + (warp * 32 + lane) * PBS;
 #pragma unroll
@@ -404,23 +463,25 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(const SolveArgs a) {
         for (int t = 0; t < TN; ++t) pb[j * TN + t] = accB[j][t];
     }
     __syncthreads();
-    for (int p = tid; p < K * nf; p += kThreads) {
-      const int k = p / nf, n = p - k * nf;
-      int kgp, jp;
-      KM::inv(k, kgp, jp);
-      const int ngp = n / TN, tp = n - ngp * TN;
-      const int cell = jp * TN + tp;
-      const int l0 = kgp + 4 * ngp;
-      float num = 0.0f, den = 0.0f;
+    for (int p = tid; p < K * NT; p += kThreads) {
+      const int k = p / NT, n = p - k * NT;  // NT is a compile-time constant
+      if (n < nf) {
+        int kgp, jp;
+        KM::inv(k, kgp, jp);
+        const int ngp = n / TN, tp = n - ngp * TN;
+        const float* p0 = UN + (kgp + 4 * ngp) * PBS + jp * TN + tp;
+        float num = 0.0f, den = 0.0f;
 #pragma unroll
-      for (int w = 0; w < kWarps; ++w) {
-        num += UN[(w * 32 + l0) * PBS + cell];
-        den += UN[(w * 32 + l0 + 16) * PBS + cell];
+        for (int w = 0; w < kWarps; ++w) {
+          num += p0[w * 32 * PBS];
+          den += p0[(w * 32 + 16) * PBS];
+        }
+        float& h = Hs[n * KP + k];
+        h = h * sqrtf(num / den);
       }
-      float& h = Hs[n * KP + k];
-      h = h * sqrtf(num / den);
     }
     __syncthreads();
+    PROF_MARK(4);  // partials + MM update
   }
 
   if (a.do_stats) {
@@ -428,49 +489,55 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(const SolveArgs a) {
     const int rgs = lane & 7, kgs = lane >> 3;
     for (int c0 = r0; c0 < r1; c0 += kChunk) {
       const int rows = min(kChunk, r1 - c0);
-      phase_a<TK, TN>(Ws, Hs, QR, fptr, WS, c0, rows, nf, eps, want_div, lane, divacc);
+      phase_a<TK, TN>(Ws, Hs, QR, fptr, c0, rows, nf, eps, lane, vv);
+      if (rows == kChunk) load_v<TN>(vv, fptr, next_full(c0), nf, lane);
       __syncwarp();
-      if (!a.stats) continue;
-      // ---------------- statistics: sa[f,k] = sum_n q[f,n] h[k,n], sb with r
-      float sa[4][TK], sb[4][TK];
+      if (want_div) divacc += chunk_divergence<TN>(QR, rows, nf, lane);
+      PROF_MARK(5);  // stats pass phase A + divergence
+      if (a.stats) {
+        // statistics: sa[f,k] = sum_n q[f,n] h[k,n], sb[f,k] = sum_n r[f,n] h[k,n]
+        float sa[4][TK], sb[4][TK];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < TK; ++j) sa[i][j] = sb[i][j] = 0.0f;
-      const int islots = (rows + 7) / 8;
-      for (int n = 0; n < nf; ++n) {
-        float hk[TK];
-        load_wk<TK>(Hs + n * KP, kgs, hk);
-        const int off = (n / TN) * 8 + (n % TN);
+          for (int j = 0; j < TK; ++j) sa[i][j] = sb[i][j] = 0.0f;
+        const int islots = (rows + 7) / 8;
+#pragma unroll 1
+        for (int n = 0; n < nf; ++n) {
+          float hk[TK];
+          load_wk<TK>(Hs + n * KP, kgs, hk);
+          const int off = (n / TN) * 8 + (n % TN);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            if (i < islots) {
+              const float q = QR[(rgs + 8 * i) * kQS + off];
+              const float r = QR[(rgs + 8 * i) * kQS + kQR_R + off];
+#pragma unroll
+              for (int j = 0; j < TK; ++j) {
+                sa[i][j] = fmaf(q, hk[j], sa[i][j]);
+                sb[i][j] = fmaf(r, hk[j], sb[i][j]);
+              }
+            }
+          }
+        }
+        float* outA = a.stats + size_t(blockIdx.x) * 2 * F * KP;
+        float* outB = outA + size_t(F) * KP;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          if (i < islots) {
-            const float q = QR[(rgs + 8 * i) * kQS + off];
-            const float r = QR[(rgs + 8 * i) * kQS + 32 + off];
+          const int rl = rgs + 8 * i;
+          if (rl < rows) {
+            const int f = c0 + rl;
 #pragma unroll
             for (int j = 0; j < TK; ++j) {
-              sa[i][j] = fmaf(q, hk[j], sa[i][j]);
-              sb[i][j] = fmaf(r, hk[j], sb[i][j]);
+              const int k = KM::k_of(kgs, j);
+              __stcs(outA + size_t(k) * F + f, sa[i][j]);
+              __stcs(outB + size_t(k) * F + f, sb[i][j]);
             }
           }
         }
       }
-      float* outA = a.stats + size_t(blockIdx.x) * 2 * F * KP;
-      float* outB = outA + size_t(F) * KP;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int rl = rgs + 8 * i;
-        if (rl < rows) {
-          const int f = c0 + rl;
-#pragma unroll
-          for (int j = 0; j < TK; ++j) {
-            const int k = KM::k_of(kgs, j);
-            outA[size_t(f) * KP + k] = sa[i][j];
-            outB[size_t(f) * KP + k] = sb[i][j];
-          }
-        }
-      }
       __syncwarp();
+      PROF_MARK(6);  // statistics
     }
   }
 
@@ -488,9 +555,10 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(const SolveArgs a) {
 
   // final activations
   if (a.Hout || a.write_store) {
-    for (int idx = tid; idx < nf * K; idx += kThreads) {
-      const int n = idx / K, k = idx - n * K;
-      const float h = Hs[n * KP + k];
+    for (int idx = tid; idx < NT * KP; idx += kThreads) {
+      const int n = idx / KP, k = idx - n * KP;  // compile-time KP
+      if (n >= nf || k >= K) continue;
+      const float h = Hs[idx];
       if (a.Hout) a.Hout[size_t(n0 + n) * K + k] = h;
       if (a.write_store) {
         const int64_t col = a.widx ? int64_t(a.widx[n0 + n]) : (a.wbase + n0 + n) % a.wmod;
@@ -499,18 +567,23 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(const SolveArgs a) {
       }
     }
   }
+  PROF_MARK(7);  // epilogue
 }
 
 // ---------------------------------------------------------------------------
 // K2 — reduce per-CTA partials into pending; commit part 1.
+// State arrays are column-major F x K (f fastest, the reference's Eigen
+// layout); cell c = k*F + f is also the offset inside each partial plane.
+// A CTA = 32 cell quads x 8 interleaved block groups; the 8 group sums are
+// combined in fixed order through shared memory (deterministic).
 // ---------------------------------------------------------------------------
 struct ReduceArgs {
-  const float* stats;
+  const float* stats;  // [nblk][2][KP][F]
   const double* divpart;
   int nblk, F, K, KP;
   int nframes;
-  const double* W64;  // [F][K]
-  double* pa;         // pending_a [F][K]
+  const double* W64;  // F x K column-major
+  double* pa;         // pending_a
   double* pb;
   double* A;
   double* B;
@@ -521,9 +594,12 @@ struct ReduceArgs {
   const unsigned int* halt;
 };
 
-__global__ void reduce_kernel(const ReduceArgs a) {
+constexpr int kRedGroups = 8;
+
+__global__ void __launch_bounds__(256) reduce_kernel(const ReduceArgs a) {
   if (a.st->status || *a.halt) return;
-  const int cell = blockIdx.x * blockDim.x + threadIdx.x;
+  __shared__ double red[kRedGroups][32][8];
+  const int q = threadIdx.x & 31, g = threadIdx.x >> 5;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     double d = 0.0;
     for (int b = 0; b < a.nblk; ++b) d += a.divpart[b];
@@ -531,37 +607,65 @@ __global__ void reduce_kernel(const ReduceArgs a) {
     a.st->pending_count += (unsigned long long)a.nframes;
     a.st->t += (unsigned long long)a.nframes;
   }
-  if (cell >= a.F * a.K) return;
-  const int f = cell / a.K, k = cell - f * a.K;
-  const size_t off = size_t(f) * a.KP + k;
+  const int ncell = a.F * a.K;
+  const int c0 = (blockIdx.x * 32 + q) * 4;
   const size_t plane = size_t(a.F) * a.KP;
-  double sa = 0.0, sb = 0.0;
-  for (int b = 0; b < a.nblk; ++b) {
-    const float* p = a.stats + size_t(b) * 2 * plane;
-    sa += double(p[off]);
-    sb += double(p[plane + off]);
+  double sa[4] = {0.0, 0.0, 0.0, 0.0}, sb[4] = {0.0, 0.0, 0.0, 0.0};
+  if (c0 < ncell) {
+    const float* base = a.stats + c0;
+#pragma unroll 4
+    for (int b = g; b < a.nblk; b += kRedGroups) {
+      const float4 x = __ldcs(reinterpret_cast<const float4*>(base + size_t(b) * 2 * plane));
+      const float4 y = __ldcs(reinterpret_cast<const float4*>(base + size_t(b) * 2 * plane + plane));
+      sa[0] += x.x;
+      sa[1] += x.y;
+      sa[2] += x.z;
+      sa[3] += x.w;
+      sb[0] += y.x;
+      sb[1] += y.y;
+      sb[2] += y.z;
+      sb[3] += y.w;
+    }
   }
-  const double w = a.W64[cell];
-  const double pa = a.pa[cell] + w * w * sa;
-  const double pb = a.pb[cell] + sb;
-  if (!a.do_commit) {
-    a.pa[cell] = pa;
-    a.pb[cell] = pb;
-    return;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    red[g][q][e] = sa[e];
+    red[g][q][4 + e] = sb[e];
   }
-  const double An = a.rho * a.A[cell] + pa;  // rho scales the past (online.hpp:319-320)
-  const double Bn = a.rho * a.B[cell] + pb;
-  a.A[cell] = An;
-  a.B[cell] = Bn;
-  a.pa[cell] = 0.0;
-  a.pb[cell] = 0.0;
-  double wn = w;
-  if (Bn > 0.0)
-    wn = sqrt(An / Bn);
-  else if (An > 0.0)
-    atomicOr(&a.st->status, ST_INCONSISTENT);
-  if (!isfinite(wn)) atomicOr(&a.st->status, ST_NONFINITE_W);
-  a.Wtmp[cell] = wn;
+  __syncthreads();
+  if (g != 0 || c0 >= ncell) return;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    double ta = 0.0, tb = 0.0;
+#pragma unroll
+    for (int gg = 0; gg < kRedGroups; ++gg) {
+      ta += red[gg][q][e];
+      tb += red[gg][q][4 + e];
+    }
+    const int cell = c0 + e;
+    if (cell >= ncell) break;
+    const double w = a.W64[cell];
+    const double pa = a.pa[cell] + w * w * ta;
+    const double pb = a.pb[cell] + tb;
+    if (!a.do_commit) {
+      a.pa[cell] = pa;
+      a.pb[cell] = pb;
+      continue;
+    }
+    const double An = a.rho * a.A[cell] + pa;  // rho scales the past (online.hpp:319-320)
+    const double Bn = a.rho * a.B[cell] + pb;
+    a.A[cell] = An;
+    a.B[cell] = Bn;
+    a.pa[cell] = 0.0;
+    a.pb[cell] = 0.0;
+    double wn = w;
+    if (Bn > 0.0)
+      wn = sqrt(An / Bn);
+    else if (An > 0.0)
+      atomicOr(&a.st->status, ST_INCONSISTENT);
+    if (!isfinite(wn)) atomicOr(&a.st->status, ST_NONFINITE_W);
+    a.Wtmp[cell] = wn;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -593,55 +697,48 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
   return t;
 }
 
-__global__ void commit_kernel(const CommitArgs a) {
+__device__ __forceinline__ double block_sum_256(double v, double* sh) {
+  v = warp_sum_d(v);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double s = 0.0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) s += sh[w];
+  __syncthreads();
+  return s;
+}
+
+__global__ void __launch_bounds__(256) commit_kernel(const CommitArgs a) {
   if (a.st->status || *a.halt) return;
   const int k = blockIdx.x, tid = threadIdx.x;
-  __shared__ double sh[256];
-  __shared__ double s_scale;
+  __shared__ double sh[8];
+  const double* wt = a.Wtmp + size_t(k) * a.F;
   double s = 0.0;
-  for (int f = tid; f < a.F; f += blockDim.x) s += a.Wtmp[size_t(f) * a.K + k];
-  sh[tid] = s;
-  __syncthreads();
-  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-    if (tid < o) sh[tid] += sh[tid + o];
-    __syncthreads();
-  }
-  if (tid == 0) s_scale = sh[0];
-  __syncthreads();
-  const double sc = s_scale;
+  for (int f = tid; f < a.F; f += blockDim.x) s += wt[f];
+  const double sc = block_sum_256(s, sh);
   if (!(sc > 0.0)) {
     if (tid == 0) atomicOr(&a.st->status, ST_ZERO_COLUMN);
     return;
   }
   double d2 = 0.0, cw = 0.0;
+  double* w64 = a.W64 + size_t(k) * a.F;
+  double* A = a.A + size_t(k) * a.F;
+  double* B = a.B + size_t(k) * a.F;
   for (int f = tid; f < a.F; f += blockDim.x) {
-    const size_t i = size_t(f) * a.K + k;
-    const double wn = a.Wtmp[i] / sc;
-    const double d = wn - a.W64[i];
+    const double wn = wt[f] / sc;
+    const double d = wn - w64[f];
     d2 += d * d;
     cw += wn;
-    a.W64[i] = wn;
-    a.A[i] /= sc;
-    a.B[i] *= sc;
+    w64[f] = wn;
+    A[f] /= sc;
+    B[f] *= sc;
     a.W32[size_t(f) * a.WS + k] = float(wn);
   }
-  __syncthreads();
-  sh[tid] = d2;
-  __syncthreads();
-  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-    if (tid < o) sh[tid] += sh[tid + o];
-    __syncthreads();
-  }
-  if (tid == 0) a.colpart[k] = sh[0];
-  __syncthreads();
-  sh[tid] = cw;
-  __syncthreads();
-  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-    if (tid < o) sh[tid] += sh[tid + o];
-    __syncthreads();
-  }
+  d2 = block_sum_256(d2, sh);
+  cw = block_sum_256(cw, sh);
   if (tid == 0) {
-    a.colpart[a.K + k] = sh[0];
+    a.colpart[k] = d2;
+    a.colpart[a.K + k] = cw;
     if (a.scale_out) a.scale_out[k] = sc;
     const unsigned long long c = a.st->commits;
     a.P[size_t(c + 1) * a.K + k] = a.P[size_t(c) * a.K + k] * sc;
