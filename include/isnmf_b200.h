@@ -1,6 +1,6 @@
 /* isnmf_b200.h — C ABI of the B200-native online / batch Itakura-Saito NMF
  * engine (sm_100a).  This is the drop-in boundary: the C++ API in
- * include/isnmf/*.hpp (same names and signatures as the reference's
+ * include/isnmf/ headers (same names and signatures as the reference's
  * proj/include/isnmf) is a thin header-only layer over these entry points,
  * and a cgo / JNI / ctypes binding would bind exactly these symbols
  * (INTEGRATION.md).
@@ -145,6 +145,14 @@ int isnmf_online_run(isnmf_online* ctx, const float* frames, int64_t ldv, int64_
 int isnmf_online_enqueue(isnmf_online* ctx, const float* frames, int64_t ldv, int64_t n, const uint64_t* index,
                          uint64_t budget, double eta);
 int isnmf_online_synchronize(isnmf_online* ctx);
+
+/* dictionary_commit (online.hpp:318-337) now, whatever t % beta is: folds the
+ * pending statistics into A, B, refreshes and renormalises W. */
+int isnmf_online_commit(isnmf_online* ctx);
+
+/* Page-locked host staging memory (so frame uploads overlap compute). */
+void* isnmf_host_alloc(int64_t bytes);
+void isnmf_host_free(void* p);
 
 /* Trace points recorded at each commit since the last clear: samples seen,
  * mini-batch objective (last_minibatch_obj) and device timestamp (seconds

@@ -69,6 +69,9 @@ _SIGS = {
     "isnmf_online_clear_trace": ([VP], C.c_int),
     "isnmf_online_get_last_h": ([VP, VP, I64], C.c_int),
     "isnmf_online_launch_count": ([VP], I64),
+    "isnmf_online_commit": ([VP], C.c_int),
+    "isnmf_host_alloc": ([I64], VP),
+    "isnmf_host_free": ([VP], None),
     "isnmf_online_profile_begin": ([VP], C.c_int),
     "isnmf_online_profile_end": ([VP, VP, VP, VP, VP], C.c_int),
     "isnmf_batch_train": ([VP, I64, I64, I64, I64, VP, VP, U64, D, D, VP, VP, VP, VP, VP, VP], C.c_int),
@@ -79,7 +82,7 @@ def header_symbols():
     """Every function name declared in include/isnmf_b200.h."""
     import re
     txt = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:const char\*|int|int64_t)\s+(isnmf_\w+)\(", txt, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:const char\*|int|int64_t|void\*|void)\s+(isnmf_\w+)\(", txt, re.M)))
 
 
 def lib():
@@ -262,6 +265,9 @@ class Online:
         h = np.empty((self.K, n), order="F")
         _check(lib().isnmf_online_get_last_h(self._h, _p(h), n))
         return h
+
+    def commit(self):
+        _check(lib().isnmf_online_commit(self._h))
 
     def launch_count(self):
         return int(lib().isnmf_online_launch_count(self._h))

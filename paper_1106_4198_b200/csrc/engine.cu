@@ -777,6 +777,68 @@ int isnmf_online_run(isnmf_online* c, const float* frames, int64_t ldv, int64_t 
   return rc ? rc : rc2;
 }
 
+int isnmf_online_commit(isnmf_online* c) {
+  if (!c) return fail(ISNMF_E_INVALID_ARG, "NULL context");
+  ReduceArgs r{};
+  r.stats = c->stats;
+  r.divpart = c->divpart;
+  r.nblk = 0;
+  r.F = c->F;
+  r.K = c->K;
+  r.KP = c->KP;
+  r.nframes = 0;
+  r.W64 = c->W64;
+  r.pa = c->pa;
+  r.pb = c->pb;
+  r.A = c->A;
+  r.B = c->B;
+  r.Wtmp = c->Wtmp;
+  r.do_commit = 1;
+  r.rho = c->rho;
+  r.st = c->st;
+  r.halt = &c->st->halt;
+  TRY(ensure_P(c, int64_t(c->commits_host) + 2));
+  TRY(ensure_trace(c, int64_t(c->commits_host - c->trace_base) + 2));
+  reduce_kernel<<<(c->F * c->K + 127) / 128, 256, 0, c->cs>>>(r);
+  CommitArgs m{};
+  m.F = c->F;
+  m.K = c->K;
+  m.WS = c->WS;
+  m.Wtmp = c->Wtmp;
+  m.W64 = c->W64;
+  m.A = c->A;
+  m.B = c->B;
+  m.W32 = c->W32;
+  m.P = c->P;
+  m.colpart = c->colpart;
+  m.st = c->st;
+  m.halt = &c->st->halt;
+  m.eta = 0.0;
+  m.tr_t = c->tr_t;
+  m.tr_obj = c->tr_obj;
+  m.tr_ns = c->tr_ns;
+  m.tr_cap = c->tr_cap;
+  commit_kernel<<<c->K, 256, 0, c->cs>>>(m);
+  c->launches += 2;
+  c->commits_host++;
+  CU(cudaGetLastError());
+  return online_finish(c, nullptr);
+}
+
+void* isnmf_host_alloc(int64_t bytes) {
+  void* p = nullptr;
+  if (bytes <= 0 || cudaHostAlloc(&p, size_t(bytes), cudaHostAllocPortable) != cudaSuccess) {
+    cudaGetLastError();
+    fail(ISNMF_E_CUDA, "host_alloc: %lld bytes failed", (long long)bytes);
+    return nullptr;
+  }
+  return p;
+}
+
+void isnmf_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
 int isnmf_online_get_trace(isnmf_online* c, uint64_t* samples, double* obj, double* seconds, int64_t cap,
                            int64_t* n) {
   if (!c) return fail(ISNMF_E_INVALID_ARG, "NULL context");
