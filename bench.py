@@ -129,6 +129,15 @@ def roofline_peak():
     return FP32_PEAK_FALLBACK
 
 
+def k1_traffic():
+    """DRAM bytes per K1 launch from the committed ncu --set full capture (or None)."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "k1_traffic.json")))
+        return d["dram_bytes_read"] + d["dram_bytes_write"]
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 def cpu_baseline(cfg, v_host_cols, w0, a0, threads, batches):
     """Oracle online pass over a bounded prefix (`batches` mini-batches)."""
     import oracle as O
@@ -295,7 +304,9 @@ def run_engine(args, rank, world):
                            "global_batch": beta, "parallelism": "replicas" if world > 1 else "single",
                            "l2": "inputs larger than L2 (V = %.2f GB fp32)" % (N * F * 4 / 1e9)},
                 "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                             "frac": achieved / peak, "traffic": None,
+                             "frac": achieved / peak, "traffic": k1_traffic(),
+                             "traffic_unit": "bytes per launch (ncu dram__bytes_read+write)",
+                             "algorithmic_bytes_per_launch": frames_per_launch * (4 * F + 8 * K),
                              "kernel": "solve_kernel<13,7>", "ms_per_launch": k1_ms,
                              "flops_per_launch": flops_per_frame * frames_per_launch,
                              "k1_share_of_step": kstats["solve_ms"] / ms_total,
