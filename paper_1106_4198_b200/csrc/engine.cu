@@ -105,6 +105,8 @@ int smem_optin() {
 }
 
 int ws_for(int KP) { return ((KP / 4) % 2 == 1) ? KP : KP + 4; }
+int row_blocks(int F) { return (F + kCellsPerCta - 1) / kCellsPerCta; }
+int padded_f(int F) { return (F + 3) & ~3; }
 
 // Picks the variant for (F, K, frames per mini-batch).
 int pick_variant(int64_t F, int64_t K, int64_t frames, Variant** out, int* WS, size_t* smem) {
@@ -376,7 +378,9 @@ int launch_block(isnmf_online* c, const float* dv, int64_t ldv, int nb, const ui
   ReduceArgs r{};
   r.stats = c->stats;
   r.divpart = c->divpart;
-  r.nblk = nblk;
+  r.nstat = nblk;
+  r.ndiv = nblk;
+  r.colpart = c->colpart;
   r.F = c->F;
   r.K = c->K;
   r.KP = c->KP;
@@ -391,7 +395,7 @@ int launch_block(isnmf_online* c, const float* dv, int64_t ldv, int nb, const ui
   r.rho = c->rho;
   r.st = c->st;
   r.halt = &c->st->halt;
-  reduce_kernel<<<(c->F * c->K + 127) / 128, 256, 0, c->cs>>>(r);
+  reduce_kernel<<<c->K * row_blocks(c->F), kRedThreads, 0, c->cs>>>(r);
   c->launches += 2;
   if (commit) {
     CommitArgs m{};
@@ -405,6 +409,7 @@ int launch_block(isnmf_online* c, const float* dv, int64_t ldv, int nb, const ui
     m.W32 = c->W32;
     m.P = c->P;
     m.colpart = c->colpart;
+    m.cta_part = c->colpart + size_t(c->K) * row_blocks(c->F);
     m.st = c->st;
     m.halt = &c->st->halt;
     m.eta = c->eta;
@@ -413,7 +418,7 @@ int launch_block(isnmf_online* c, const float* dv, int64_t ldv, int nb, const ui
     m.tr_ns = c->tr_ns;
     m.tr_cap = c->tr_cap;
     m.batch_mode = 0;
-    commit_kernel<<<c->K, 256, 0, c->cs>>>(m);
+    commit_kernel<<<c->K * row_blocks(c->F), kCellsPerCta, 0, c->cs>>>(m);
     c->launches++;
     c->commits_host++;
   }
@@ -582,9 +587,10 @@ int isnmf_online_create(isnmf_online** out, const isnmf_online_config* cfg) {
                      cudaGetErrorString(cudaGetLastError())));
   if ((rc = dalloc(&c->st, 1)) || (rc = dalloc(&c->W64, FK)) || (rc = dalloc(&c->A, FK)) ||
       (rc = dalloc(&c->B, FK)) || (rc = dalloc(&c->pa, FK)) || (rc = dalloc(&c->pb, FK)) ||
-      (rc = dalloc(&c->Wtmp, FK)) || (rc = dalloc(&c->colpart, 2 * size_t(c->K))) ||
+      (rc = dalloc(&c->Wtmp, FK)) || (rc = dalloc(&c->colpart, 3 * size_t(c->K) * row_blocks(c->F))) ||
       (rc = dalloc(&c->W32, size_t(c->F) * c->WS)) ||
-      (rc = dalloc(&c->stats, size_t(c->maxblk) * 2 * c->F * c->KP + 4)) || (rc = dalloc(&c->divpart, c->maxblk)) ||
+      (rc = dalloc(&c->stats, size_t(c->maxblk) * 2 * padded_f(c->F) * c->KP + 4)) ||
+      (rc = dalloc(&c->divpart, c->maxblk)) ||
       (rc = dalloc(&c->Hlast, size_t(c->beta) * c->K)))
     return bail(rc);
   if (c->restart == ISNMF_RESTART_FRESH && (rc = dalloc(&c->u01, size_t(c->beta) * c->K))) return bail(rc);
@@ -786,7 +792,9 @@ int isnmf_online_commit(isnmf_online* c) {
   ReduceArgs r{};
   r.stats = c->stats;
   r.divpart = c->divpart;
-  r.nblk = 0;
+  r.nstat = 0;
+  r.ndiv = 0;
+  r.colpart = c->colpart;
   r.F = c->F;
   r.K = c->K;
   r.KP = c->KP;
@@ -803,7 +811,7 @@ int isnmf_online_commit(isnmf_online* c) {
   r.halt = &c->st->halt;
   TRY(ensure_P(c, int64_t(c->commits_host) + 2));
   TRY(ensure_trace(c, int64_t(c->commits_host - c->trace_base) + 2));
-  reduce_kernel<<<(c->F * c->K + 127) / 128, 256, 0, c->cs>>>(r);
+  reduce_kernel<<<c->K * row_blocks(c->F), kRedThreads, 0, c->cs>>>(r);
   CommitArgs m{};
   m.F = c->F;
   m.K = c->K;
@@ -815,6 +823,7 @@ int isnmf_online_commit(isnmf_online* c) {
   m.W32 = c->W32;
   m.P = c->P;
   m.colpart = c->colpart;
+  m.cta_part = c->colpart + size_t(c->K) * row_blocks(c->F);
   m.st = c->st;
   m.halt = &c->st->halt;
   m.eta = 0.0;
@@ -822,7 +831,7 @@ int isnmf_online_commit(isnmf_online* c) {
   m.tr_obj = c->tr_obj;
   m.tr_ns = c->tr_ns;
   m.tr_cap = c->tr_cap;
-  commit_kernel<<<c->K, 256, 0, c->cs>>>(m);
+  commit_kernel<<<c->K * row_blocks(c->F), kCellsPerCta, 0, c->cs>>>(m);
   c->launches += 2;
   c->commits_host++;
   CU(cudaGetLastError());
@@ -1035,10 +1044,10 @@ struct SolveWork {
     TRY(dalloc(&A, FK));
     TRY(dalloc(&B, FK));
     TRY(dalloc(&Wtmp, FK));
-    TRY(dalloc(&colpart, 2 * size_t(K)));
+    TRY(dalloc(&colpart, 3 * size_t(K) * row_blocks(F)));
     TRY(dalloc(&P, 2 * size_t(K)));
     TRY(dalloc(&scale, size_t(K)));
-    TRY(dalloc(&stats, size_t(seg_blocks) * 2 * F * KP + 4));
+    TRY(dalloc(&stats, size_t(seg_blocks) * 2 * padded_f(F) * KP + 4));
     TRY(dalloc(&divpart, size_t(seg_blocks)));
     TRY(dalloc(&halt, 1));
     CU(cudaMemset(halt, 0, sizeof(unsigned int)));
@@ -1096,7 +1105,9 @@ struct SolveWork {
       ReduceArgs r{};
       r.stats = stats;
       r.divpart = divpart;
-      r.nblk = stats_on ? nblk : 0;
+      r.nstat = stats_on ? nblk : 0;
+      r.ndiv = nblk;
+      r.colpart = colpart;
       r.F = F;
       r.K = K;
       r.KP = KP;
@@ -1107,14 +1118,7 @@ struct SolveWork {
       r.do_commit = 0;
       r.st = st;
       r.halt = halt;
-      if (!stats_on) {  // divergence only: fold divpart with a 1-thread reduce
-        r.F = 0;
-        r.nblk = 0;
-      }
-      // divergence partials are always folded (reduce_kernel block 0 sums divpart[0..nblk_div))
-      r.nblk = nblk;
-      if (!stats_on) r.F = 0;
-      reduce_kernel<<<std::max(1, (r.F * K + 127) / 128), 256, 0, s>>>(r);
+      reduce_kernel<<<K * row_blocks(F), kRedThreads, 0, s>>>(r);
       CU(cudaGetLastError());
     }
     return 0;
@@ -1347,7 +1351,9 @@ int isnmf_batch_train(const float* v, int64_t ldv, int64_t F, int64_t N, int64_t
     ReduceArgs r{};
     r.stats = wk.stats;
     r.divpart = wk.divpart;
-    r.nblk = 0;
+    r.nstat = 0;
+    r.ndiv = 0;
+    r.colpart = wk.colpart;
     r.F = int(F);
     r.K = int(K);
     r.KP = wk.KP;
@@ -1362,7 +1368,7 @@ int isnmf_batch_train(const float* v, int64_t ldv, int64_t F, int64_t N, int64_t
     r.rho = 0.0;
     r.st = wk.st;
     r.halt = wk.halt;
-    reduce_kernel<<<int((F * K + 127) / 128), 256, 0, wk.s>>>(r);
+    reduce_kernel<<<int(K) * row_blocks(int(F)), kRedThreads, 0, wk.s>>>(r);
     CommitArgs m{};
     m.F = int(F);
     m.K = int(K);
@@ -1374,12 +1380,13 @@ int isnmf_batch_train(const float* v, int64_t ldv, int64_t F, int64_t N, int64_t
     m.W32 = wk.W32;
     m.P = wk.P;
     m.colpart = wk.colpart;
+    m.cta_part = wk.colpart + size_t(K) * row_blocks(int(F));
     m.st = wk.st;
     m.halt = wk.halt;
     m.scale_out = dscale;
     m.batch_mode = 1;
     // commit_kernel indexes P by st->commits: keep commits at 0 (2-row P)
-    commit_kernel<<<int(K), 256, 0, wk.s>>>(m);
+    commit_kernel<<<int(K) * row_blocks(int(F)), kCellsPerCta, 0, wk.s>>>(m);
     CU(cudaGetLastError());
     DevState h{};
     TRY(wk.state(&h));

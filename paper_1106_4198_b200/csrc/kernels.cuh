@@ -145,7 +145,7 @@ struct SolveArgs {
   int do_stats;   // extra pass with the final h: divergence (+ statistics when stats != nullptr)
   int div_first;  // divergence from pass 0 (the incoming h) instead of the final pass
   int check_h0;   // flag h0 <= 0 as NonPositiveInit (solve_h, kernels.hpp:67)
-  float* stats;     // [gridDim][2][KP][F]
+  float* stats;     // [gridDim][2][KP][FP], FP = F rounded up to 4
   double* divpart;  // [gridDim]
   unsigned int* status;
   const unsigned int* halt;
@@ -349,11 +349,22 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(const SolveArgs a) {
   const int nf = min(NT, a.nframes - n0);
   PROF_T0();
 
-  {  // dictionary -> smem (row stride WS, pads are zero in W32)
-    const float4* src = reinterpret_cast<const float4*>(a.W32);
-    float4* dst = reinterpret_cast<float4*>(Ws);
-    const int n4 = F * WS / 4;
-    for (int i = tid; i < n4; i += kThreads) dst[i] = __ldg(src + i);
+  __shared__ __align__(8) unsigned long long wbar;
+  if (tid == 0) {  // dictionary -> smem by TMA bulk copies, overlapped with the h0 set-up below
+    const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&wbar));
+    const uint32_t bytes = uint32_t(F) * WS * 4u;  // multiple of 16 (WS % 4 == 0)
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes));
+    const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(Ws));
+    constexpr uint32_t kPiece = 32768;
+    for (uint32_t off = 0; off < bytes; off += kPiece) {
+      const uint32_t n = bytes - off < kPiece ? bytes - off : kPiece;
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       dst + off),
+                   "l"(reinterpret_cast<const char*>(a.W32) + off), "r"(n), "r"(bar)
+                   : "memory");
+    }
   }
   if (tid < NT) {
     const int64_t fr = tid < nf ? (a.vsel ? a.vsel[n0 + tid] : a.v0 + n0 + tid) : 0;
@@ -392,6 +403,16 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(const SolveArgs a) {
       if (a.check_h0 && !(val > 0.0f)) s_bad = 1;
     }
     Hs[idx] = val;
+  }
+  {  // wait for the dictionary (phase 0 of wbar)
+    const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&wbar));
+    uint32_t done = 0;
+    while (!done)
+      asm volatile(
+          "{\n\t.reg .pred P;\n\tmbarrier.try_wait.parity.shared::cta.b64 P, [%1], 0;\n\tselp.b32 %0, 1, 0, P;\n\t}\n"
+          : "=r"(done)
+          : "r"(bar)
+          : "memory");
   }
   __syncthreads();
   if (s_bad) {
@@ -520,8 +541,9 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(const SolveArgs a) {
             }
           }
         }
-        float* outA = a.stats + size_t(blockIdx.x) * 2 * F * KP;
-        float* outB = outA + size_t(F) * KP;
+        const int FP = (F + 3) & ~3;  // partial planes padded so K2 can read float4 quads
+        float* outA = a.stats + size_t(blockIdx.x) * 2 * FP * KP;
+        float* outB = outA + size_t(FP) * KP;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int rl = rgs + 8 * i;
@@ -530,8 +552,8 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(const SolveArgs a) {
 #pragma unroll
             for (int j = 0; j < TK; ++j) {
               const int k = KM::k_of(kgs, j);
-              __stcs(outA + size_t(k) * F + f, sa[i][j]);
-              __stcs(outB + size_t(k) * F + f, sb[i][j]);
+              outA[size_t(k) * FP + f] = sa[i][j];
+              outB[size_t(k) * FP + f] = sb[i][j];
             }
           }
         }
@@ -574,13 +596,15 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(const SolveArgs a) {
 // K2 — reduce per-CTA partials into pending; commit part 1.
 // State arrays are column-major F x K (f fastest, the reference's Eigen
 // layout); cell c = k*F + f is also the offset inside each partial plane.
-// A CTA = 32 cell quads x 8 interleaved block groups; the 8 group sums are
-// combined in fixed order through shared memory (deterministic).
+// A CTA = (column k, 128-row block) = 32 row quads x 16 interleaved partial
+// groups; the group sums are combined in fixed order through shared memory.
 // ---------------------------------------------------------------------------
 struct ReduceArgs {
   const float* stats;  // [nblk][2][KP][F]
   const double* divpart;
-  int nblk, F, K, KP;
+  int nstat;  // statistics partial blocks to fold into pending (0: none)
+  int ndiv;   // divergence partials to fold into pending_div
+  int F, K, KP;
   int nframes;
   const double* W64;  // F x K column-major
   double* pa;         // pending_a
@@ -588,35 +612,42 @@ struct ReduceArgs {
   double* A;
   double* B;
   double* Wtmp;
+  double* colpart;  // [gridDim]: this CTA's fixed-order sum of W_tmp over its rows of column k
   int do_commit;
   double rho;
   DevState* st;
   const unsigned int* halt;
 };
 
-constexpr int kRedGroups = 8;
+constexpr int kRedGroups = 16;                 // interleaved partial groups per cell quad
+constexpr int kRedThreads = 32 * kRedGroups;   // 512
+constexpr int kCellsPerCta = 128;              // 32 quads x 4 cells
 
-__global__ void __launch_bounds__(256) reduce_kernel(const ReduceArgs a) {
+__global__ void __launch_bounds__(kRedThreads) reduce_kernel(const ReduceArgs a) {
   if (a.st->status || *a.halt) return;
   __shared__ double red[kRedGroups][32][8];
+  __shared__ double csum[32];
   const int q = threadIdx.x & 31, g = threadIdx.x >> 5;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     double d = 0.0;
-    for (int b = 0; b < a.nblk; ++b) d += a.divpart[b];
+    for (int b = 0; b < a.ndiv; ++b) d += a.divpart[b];
     a.st->pending_div += d;
     a.st->pending_count += (unsigned long long)a.nframes;
     a.st->t += (unsigned long long)a.nframes;
   }
-  const int ncell = a.F * a.K;
-  const int c0 = (blockIdx.x * 32 + q) * 4;
-  const size_t plane = size_t(a.F) * a.KP;
+  // CTA = (column k, block of 128 rows); quad q = rows f0 .. f0+3
+  const int nrb = (a.F + kCellsPerCta - 1) / kCellsPerCta;
+  const int k = blockIdx.x / nrb, rb = blockIdx.x - k * nrb;
+  const int f0 = rb * kCellsPerCta + q * 4;
+  const int FP = (a.F + 3) & ~3;
+  const size_t plane = size_t(FP) * a.KP;
   double sa[4] = {0.0, 0.0, 0.0, 0.0}, sb[4] = {0.0, 0.0, 0.0, 0.0};
-  if (c0 < ncell) {
-    const float* base = a.stats + c0;
+  if (f0 < a.F) {
+    const float* base = a.stats + size_t(k) * FP + f0;
 #pragma unroll 4
-    for (int b = g; b < a.nblk; b += kRedGroups) {
-      const float4 x = __ldcs(reinterpret_cast<const float4*>(base + size_t(b) * 2 * plane));
-      const float4 y = __ldcs(reinterpret_cast<const float4*>(base + size_t(b) * 2 * plane + plane));
+    for (int b = g; b < a.nstat; b += kRedGroups) {
+      const float4 x = __ldcg(reinterpret_cast<const float4*>(base + size_t(b) * 2 * plane));
+      const float4 y = __ldcg(reinterpret_cast<const float4*>(base + size_t(b) * 2 * plane + plane));
       sa[0] += x.x;
       sa[1] += x.y;
       sa[2] += x.z;
@@ -633,53 +664,68 @@ __global__ void __launch_bounds__(256) reduce_kernel(const ReduceArgs a) {
     red[g][q][4 + e] = sb[e];
   }
   __syncthreads();
-  if (g != 0 || c0 >= ncell) return;
+  if (g == 0) {
+    double cs = 0.0;
 #pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    double ta = 0.0, tb = 0.0;
+    for (int e = 0; e < 4; ++e) {
+      double ta = 0.0, tb = 0.0;
 #pragma unroll
-    for (int gg = 0; gg < kRedGroups; ++gg) {
-      ta += red[gg][q][e];
-      tb += red[gg][q][4 + e];
+      for (int gg = 0; gg < kRedGroups; ++gg) {
+        ta += red[gg][q][e];
+        tb += red[gg][q][4 + e];
+      }
+      if (f0 + e >= a.F) break;
+      const int cell = k * a.F + f0 + e;
+      const double w = a.W64[cell];
+      const double pa = a.pa[cell] + w * w * ta;
+      const double pb = a.pb[cell] + tb;
+      if (!a.do_commit) {
+        a.pa[cell] = pa;
+        a.pb[cell] = pb;
+        continue;
+      }
+      const double An = a.rho * a.A[cell] + pa;  // rho scales the past (online.hpp:319-320)
+      const double Bn = a.rho * a.B[cell] + pb;
+      a.A[cell] = An;
+      a.B[cell] = Bn;
+      a.pa[cell] = 0.0;
+      a.pb[cell] = 0.0;
+      double wn = w;
+      if (Bn > 0.0)
+        wn = sqrt(An / Bn);
+      else if (An > 0.0)
+        atomicOr(&a.st->status, ST_INCONSISTENT);
+      if (!isfinite(wn)) atomicOr(&a.st->status, ST_NONFINITE_W);
+      a.Wtmp[cell] = wn;
+      cs += wn;
     }
-    const int cell = c0 + e;
-    if (cell >= ncell) break;
-    const double w = a.W64[cell];
-    const double pa = a.pa[cell] + w * w * ta;
-    const double pb = a.pb[cell] + tb;
-    if (!a.do_commit) {
-      a.pa[cell] = pa;
-      a.pb[cell] = pb;
-      continue;
-    }
-    const double An = a.rho * a.A[cell] + pa;  // rho scales the past (online.hpp:319-320)
-    const double Bn = a.rho * a.B[cell] + pb;
-    a.A[cell] = An;
-    a.B[cell] = Bn;
-    a.pa[cell] = 0.0;
-    a.pb[cell] = 0.0;
-    double wn = w;
-    if (Bn > 0.0)
-      wn = sqrt(An / Bn);
-    else if (An > 0.0)
-      atomicOr(&a.st->status, ST_INCONSISTENT);
-    if (!isfinite(wn)) atomicOr(&a.st->status, ST_NONFINITE_W);
-    a.Wtmp[cell] = wn;
+    if (a.do_commit) csum[q] = cs;
+  }
+  if (!a.do_commit) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {  // fixed-order partial sum of W_tmp over this CTA's rows of column k
+    double c = 0.0;
+    for (int i = 0; i < 32; ++i) c += csum[i];
+    a.colpart[blockIdx.x] = c;
   }
 }
 
 // ---------------------------------------------------------------------------
-// K3 — column renormalisation, ||dW||_F, trace point, stop rule.
+// K3 — column renormalisation, ||dW||_F, trace point, stop rule.  Same tiling
+// as K2: a CTA scales its 128 rows of column k by s_k (the K2 row-block
+// partials of column k in fixed order, identical in every CTA), and the last
+// CTA to finish folds the per-CTA ||dW||^2 and sum W in CTA order.
 // ---------------------------------------------------------------------------
 struct CommitArgs {
   int F, K, WS;
+  const double* colpart;   // [K * nrb] from K2
+  double* cta_part;        // [gridDim][2]: dW^2, sum W of this CTA
   const double* Wtmp;
   double* W64;
   double* A;
   double* B;
   float* W32;
-  double* P;       // prefix products of the column scales [commits+1][K]
-  double* colpart; // [2][K]
+  double* P;  // prefix products of the column scales [commits+1][K]
   DevState* st;
   unsigned int* halt;
   double eta;
@@ -688,7 +734,7 @@ struct CommitArgs {
   unsigned long long* tr_ns;
   long long tr_cap;
   double* scale_out;  // optional: column scales s_k of this commit (batch H compensation)
-  int batch_mode;  // 1: no eta halt here (batch stops on the host-visible epoch)
+  int batch_mode;
 };
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
@@ -697,63 +743,89 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
   return t;
 }
 
-__device__ __forceinline__ double block_sum_256(double v, double* sh) {
-  v = warp_sum_d(v);
-  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
-  __syncthreads();
+// s_k: the K2 row-block partials of column k summed in row-block order.
+__device__ __forceinline__ double column_scale(const double* colpart, int nrb, int k) {
   double s = 0.0;
-#pragma unroll
-  for (int w = 0; w < 8; ++w) s += sh[w];
-  __syncthreads();
+  for (int rb = 0; rb < nrb; ++rb) s += colpart[k * nrb + rb];
   return s;
 }
 
-__global__ void __launch_bounds__(256) commit_kernel(const CommitArgs a) {
+__global__ void __launch_bounds__(kCellsPerCta) commit_kernel(const CommitArgs a) {
   if (a.st->status || *a.halt) return;
-  const int k = blockIdx.x, tid = threadIdx.x;
-  __shared__ double sh[8];
-  const double* wt = a.Wtmp + size_t(k) * a.F;
-  double s = 0.0;
-  for (int f = tid; f < a.F; f += blockDim.x) s += wt[f];
-  const double sc = block_sum_256(s, sh);
-  if (!(sc > 0.0)) {
-    if (tid == 0) atomicOr(&a.st->status, ST_ZERO_COLUMN);
-    return;
-  }
+  __shared__ double sh_d[kCellsPerCta / 32], sh_w[kCellsPerCta / 32];
+  __shared__ int s_bad, s_last;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nrb = (a.F + kCellsPerCta - 1) / kCellsPerCta;
+  const int k = blockIdx.x / nrb, f = (blockIdx.x - k * nrb) * kCellsPerCta + tid;
+  const int cell = k * a.F + f;
+  if (tid == 0) s_bad = 0;
+  __syncthreads();
   double d2 = 0.0, cw = 0.0;
-  double* w64 = a.W64 + size_t(k) * a.F;
-  double* A = a.A + size_t(k) * a.F;
-  double* B = a.B + size_t(k) * a.F;
-  for (int f = tid; f < a.F; f += blockDim.x) {
-    const double wn = wt[f] / sc;
-    const double d = wn - w64[f];
-    d2 += d * d;
-    cw += wn;
-    w64[f] = wn;
-    A[f] /= sc;
-    B[f] *= sc;
-    a.W32[size_t(f) * a.WS + k] = float(wn);
+  if (f < a.F) {
+    const double sc = column_scale(a.colpart, nrb, k);
+    if (!(sc > 0.0)) {
+      s_bad = 1;
+    } else {
+      const double wn = a.Wtmp[cell] / sc;
+      const double d = wn - a.W64[cell];
+      d2 = d * d;
+      cw = wn;
+      a.W64[cell] = wn;
+      a.A[cell] /= sc;
+      a.B[cell] *= sc;
+      a.W32[size_t(f) * a.WS + k] = float(wn);
+      if (f == 0) {
+        const unsigned long long c = a.st->commits;
+        a.P[size_t(c + 1) * a.K + k] = a.P[size_t(c) * a.K + k] * sc;
+        if (a.scale_out) a.scale_out[k] = sc;
+      }
+    }
   }
-  d2 = block_sum_256(d2, sh);
-  cw = block_sum_256(cw, sh);
+  d2 = warp_sum_d(d2);
+  cw = warp_sum_d(cw);
+  if (lane == 0) {
+    sh_d[warp] = d2;
+    sh_w[warp] = cw;
+  }
+  __syncthreads();
   if (tid == 0) {
-    a.colpart[k] = d2;
-    a.colpart[a.K + k] = cw;
-    if (a.scale_out) a.scale_out[k] = sc;
-    const unsigned long long c = a.st->commits;
-    a.P[size_t(c + 1) * a.K + k] = a.P[size_t(c) * a.K + k] * sc;
+    if (s_bad) atomicOr(&a.st->status, ST_ZERO_COLUMN);
+    double dd = 0.0, ww = 0.0;
+    for (int w = 0; w < kCellsPerCta / 32; ++w) {
+      dd += sh_d[w];
+      ww += sh_w[w];
+    }
+    a.cta_part[2 * blockIdx.x] = dd;
+    a.cta_part[2 * blockIdx.x + 1] = ww;
     __threadfence();
-    const unsigned int ticket = atomicAdd(&a.st->ticket, 1u);
-    if (ticket == unsigned(a.K - 1)) {  // last column done: scalar epilogue
-      __threadfence();
-      double dd = 0.0, ww = 0.0;
-      for (int kk = 0; kk < a.K; ++kk) {
-        dd += ((volatile double*)a.colpart)[kk];
-        ww += ((volatile double*)a.colpart)[a.K + kk];
+    s_last = atomicAdd(&a.st->ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last) {  // last CTA: fold the per-CTA partials (fixed order: strided per thread, then by warp)
+    __threadfence();
+    double pd = 0.0, pw = 0.0;
+    for (unsigned int b = tid; b < gridDim.x; b += kCellsPerCta) {
+      pd += __ldcg(a.cta_part + 2 * b);
+      pw += __ldcg(a.cta_part + 2 * b + 1);
+    }
+    pd = warp_sum_d(pd);
+    pw = warp_sum_d(pw);
+    __syncthreads();
+    if (lane == 0) {
+      sh_d[warp] = pd;
+      sh_w[warp] = pw;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double sd = 0.0, sw = 0.0;
+      for (int w = 0; w < kCellsPerCta / 32; ++w) {
+        sd += sh_d[w];
+        sw += sh_w[w];
       }
       DevState* st = a.st;
-      st->last_delta = sqrt(dd);
-      st->kmeanw = double(a.K) * (ww / (double(a.F) * double(a.K)));
+      const unsigned long long c = st->commits;
+      st->last_delta = sqrt(sd);
+      st->kmeanw = double(a.K) * (sw / (double(a.F) * double(a.K)));
       st->last_obj = st->pending_count ? st->pending_div / double(st->pending_count) : 0.0;
       const long long ti = (long long)(c - st->trace_base);
       if (a.tr_t && ti >= 0 && ti < a.tr_cap) {
