@@ -49,8 +49,11 @@ typedef enum isnmf_status {
   ISNMF_E_UNSUPPORTED = 22        /* shape outside the built kernel family */
 } isnmf_status;
 
-/* Restart modes (model.hpp:20-30) plus the engine's constant-h0 reading. */
+/* Restart modes (model.hpp:20-30). */
 enum { ISNMF_RESTART_WARM = 0, ISNMF_RESTART_FRESH = 1 };
+/* Engine flags: force the generic (W-streaming) solve kernel even when a
+ * register-tiled variant would fit (testing / comparison). */
+enum { ISNMF_FLAG_GENERIC_SOLVE = 1 };
 
 const char* isnmf_last_error(void);
 /* Library / device description: writes a short JSON string. */
@@ -101,7 +104,7 @@ typedef struct isnmf_online_config {
   int32_t inner_iters;   /* effective H iterations per visit (>= 1) */
   double epsilon;        /* SolverConfig::epsilon */
   int32_t restart;       /* ISNMF_RESTART_WARM / ISNMF_RESTART_FRESH */
-  int32_t reserved;
+  int32_t flags;         /* ISNMF_FLAG_* */
   uint64_t seed;         /* SolverConfig::seed (fresh-restart stream) */
   int64_t n_store;       /* warm mode: columns of the activation store (dataset size) */
   int64_t max_chunk;     /* frames per H2D chunk when streaming host frames (0 = 64*beta) */

@@ -35,7 +35,7 @@ class EngineError(RuntimeError):
 
 class OnlineConfig(C.Structure):
     _fields_ = [("F", C.c_int64), ("K", C.c_int64), ("beta", C.c_int32), ("inner_iters", C.c_int32),
-                ("epsilon", C.c_double), ("restart", C.c_int32), ("reserved", C.c_int32), ("seed", C.c_uint64),
+                ("epsilon", C.c_double), ("restart", C.c_int32), ("flags", C.c_int32), ("seed", C.c_uint64),
                 ("n_store", C.c_int64), ("max_chunk", C.c_int64)]
 
 
@@ -176,9 +176,10 @@ def rescale_dictionary(w, a, b, warm_h=None):
 class Online:
     """Device-resident OnlineState (online.hpp:224-248) behind the C ABI."""
 
-    def __init__(self, F, K, beta, inner_iters, epsilon=1e-12, restart="warm", seed=1, n_store=0, max_chunk=0):
+    def __init__(self, F, K, beta, inner_iters, epsilon=1e-12, restart="warm", seed=1, n_store=0, max_chunk=0,
+                 generic=False):
         cfg = OnlineConfig(F=F, K=K, beta=beta, inner_iters=inner_iters, epsilon=epsilon, restart=RESTART[restart],
-                           seed=seed, n_store=n_store, max_chunk=max_chunk)
+                           seed=seed, n_store=n_store, max_chunk=max_chunk, flags=1 if generic else 0)
         h = C.c_void_p()
         _check(lib().isnmf_online_create(C.byref(h), C.byref(cfg)))
         self._h = h

@@ -124,7 +124,7 @@ int pick_variant(int64_t F, int64_t K, int64_t frames, Variant** out, int* WS, s
       if (!best || v.TK < best->TK || (v.TK == best->TK && v.TN > best->TN)) best = &v;
     }
   }
-  if (!best) return fail(ISNMF_E_UNSUPPORTED, "K=%lld exceeds the built kernel family (K <= 64)", (long long)K);
+  if (!best) return 1;  // no register-tiled variant: caller uses the generic kernel
   const int w = ws_for(4 * best->TK);
   if (!best->configured) {
     cudaFuncAttributes at;
@@ -135,13 +135,63 @@ int pick_variant(int64_t F, int64_t K, int64_t frames, Variant** out, int* WS, s
     best->configured = true;
   }
   const size_t sm = best->smem(int(F));
-  if (sm + best->static_smem > size_t(smem_optin()))
-    return fail(ISNMF_E_UNSUPPORTED, "F=%lld, K=%lld: dictionary (%zu B) does not fit shared memory", (long long)F,
-                (long long)K, sm);
+  if (sm + best->static_smem > size_t(smem_optin())) return 1;  // W does not fit: generic kernel
   *out = best;
   *WS = w;
   *smem = sm;
   return 0;
+}
+
+// Solve-kernel choice for (F, K, frames per batch): a register-tiled variant when
+// W fits shared memory, else the generic streaming kernel.
+struct SolvePlan {
+  Variant* var = nullptr;  // nullptr: generic
+  int NT = 0, KP = 0, WS = 0;
+  size_t smem = 0;
+};
+
+bool generic_configured = false;
+
+int plan_solve(int64_t F, int64_t K, int64_t frames, SolvePlan* plan, bool force_generic = false) {
+  Variant* v = nullptr;
+  int WS = 0;
+  size_t sm = 0;
+  const int rc = force_generic ? 1 : pick_variant(F, K, frames, &v, &WS, &sm);
+  if (rc == 0) {
+    plan->var = v;
+    plan->NT = 4 * v->TN;
+    plan->KP = 4 * v->TK;
+    plan->WS = WS;
+    plan->smem = sm;
+    return 0;
+  }
+  if (rc != 1) return rc;
+  const int64_t per_cta = (frames + device_sms() - 1) / device_sms();
+  int nt = int(std::min<int64_t>(64, std::max<int64_t>(1, per_cta)));
+  while (nt > 1 && K * nt > int64_t(kGenThreads) * kGenMaxPairs) --nt;
+  if (K * nt > int64_t(kGenThreads) * kGenMaxPairs)
+    return fail(ISNMF_E_UNSUPPORTED, "K=%lld too large for the generic kernel", (long long)K);
+  const GenShape G(nt, int(K));
+  const size_t smem = G.smem_floats() * sizeof(float);
+  if (!generic_configured) {
+    CU(cudaFuncSetAttribute(solve_generic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin() - 2048));
+    generic_configured = true;
+  }
+  if (smem + 2048 > size_t(smem_optin()))
+    return fail(ISNMF_E_UNSUPPORTED, "K=%lld: generic kernel needs %zu B of shared memory", (long long)K, smem);
+  plan->var = nullptr;
+  plan->NT = nt;
+  plan->KP = G.KP;
+  plan->WS = G.WS;
+  plan->smem = smem;
+  return 0;
+}
+
+void launch_solve(const SolvePlan& p, int nblk, const SolveArgs& a, cudaStream_t s) {
+  if (p.var)
+    p.var->fn<<<nblk, kThreads, p.smem, s>>>(a);
+  else
+    solve_generic_kernel<<<nblk, kGenThreads, p.smem, s>>>(a, p.NT);
 }
 
 template <class T>
@@ -216,9 +266,8 @@ struct isnmf_online {
   isnmf_online_config cfg{};
   int F = 0, K = 0, beta = 0, iters = 0, restart = 0;
   double eps = 0.0;
-  Variant* var = nullptr;
+  SolvePlan plan;
   int WS = 0, KP = 0, NT = 0;
-  size_t smem = 0;
   cudaStream_t cs = nullptr, xs = nullptr;
   DevState* st = nullptr;
   double *W64 = nullptr, *A = nullptr, *B = nullptr, *pa = nullptr, *pb = nullptr, *Wtmp = nullptr;
@@ -368,7 +417,7 @@ int launch_block(isnmf_online* c, const float* dv, int64_t ldv, int nb, const ui
     }
     CU(cudaEventRecord(c->ev_pool[c->ev_used], c->cs));
   }
-  c->var->fn<<<nblk, kThreads, c->smem, c->cs>>>(a);
+  launch_solve(c->plan, nblk, a, c->cs);
   if (c->prof) {
     CU(cudaEventRecord(c->ev_pool[c->ev_used + 1], c->cs));
     c->ev_used += 2;
@@ -569,7 +618,7 @@ int isnmf_online_create(isnmf_online** out, const isnmf_online_config* cfg) {
   c->eps = cfg->epsilon;
   c->nstore = cfg->restart == ISNMF_RESTART_WARM ? cfg->n_store : 0;
   c->chunk = cfg->max_chunk > 0 ? cfg->max_chunk : int64_t(64) * cfg->beta;
-  int rc = pick_variant(c->F, c->K, c->beta, &c->var, &c->WS, &c->smem);
+  int rc = plan_solve(c->F, c->K, c->beta, &c->plan, (cfg->flags & ISNMF_FLAG_GENERIC_SOLVE) != 0);
   auto bail = [&](int code) {
     std::string keep = g_err;
     online_free(c);
@@ -577,8 +626,9 @@ int isnmf_online_create(isnmf_online** out, const isnmf_online_config* cfg) {
     return code;
   };
   if (rc) return bail(rc);
-  c->KP = 4 * c->var->TK;
-  c->NT = 4 * c->var->TN;
+  c->KP = c->plan.KP;
+  c->NT = c->plan.NT;
+  c->WS = c->plan.WS;
   c->maxblk = (c->beta + c->NT - 1) / c->NT;
   const size_t FK = size_t(c->F) * c->K;
   if (cudaStreamCreateWithFlags(&c->cs, cudaStreamNonBlocking) != cudaSuccess ||
@@ -1007,8 +1057,7 @@ __global__ void rescale_kernel(double* w, double* a, double* b, int64_t F, int64
 // A device workspace for the fused solve over an arbitrary set of frames.
 struct SolveWork {
   int F = 0, K = 0, WS = 0, KP = 0, NT = 0;
-  Variant* var = nullptr;
-  size_t smem = 0;
+  SolvePlan plan;
   int seg_blocks = 0;
   cudaStream_t s = nullptr;
   DevState* st = nullptr;
@@ -1030,9 +1079,10 @@ struct SolveWork {
   int init(int64_t F_, int64_t K_, int64_t frames) {
     F = int(F_);
     K = int(K_);
-    TRY(pick_variant(F, K, frames, &var, &WS, &smem));
-    KP = 4 * var->TK;
-    NT = 4 * var->TN;
+    TRY(plan_solve(F, K, frames, &plan));
+    KP = plan.KP;
+    NT = plan.NT;
+    WS = plan.WS;
     seg_blocks = device_sms() * 4;
     CU(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     const size_t FK = size_t(F) * K;
@@ -1101,7 +1151,7 @@ struct SolveWork {
       a.divpart = divpart;
       a.status = &st->status;
       a.halt = halt;
-      var->fn<<<nblk, kThreads, smem, s>>>(a);
+      launch_solve(plan, nblk, a, s);
       ReduceArgs r{};
       r.stats = stats;
       r.divpart = divpart;

@@ -888,3 +888,192 @@ __global__ void fresh_kernel(uint64_t seed, uint64_t t0, int n, int K, double* u
 }
 
 }  // namespace isnmf_dev
+
+namespace isnmf_dev {
+
+// ---------------------------------------------------------------------------
+// K1g — generic solve for any K (used when W does not fit shared memory, e.g.
+// config 4: F = 1025, K = 256).  W is streamed through shared memory in
+// 32-row chunks every pass; each thread keeps num / den of its (k, n) pairs in
+// registers.  Same inputs / outputs as solve_kernel (stats partials
+// [CTA][2][KP][FP], divergence partials, H out / warm store).
+// ---------------------------------------------------------------------------
+constexpr int kGenThreads = 512;
+constexpr int kGenChunk = 32;
+constexpr int kGenMaxPairs = 32;  // (k, n) pairs per thread: K * NT <= 512 * 32
+
+struct GenShape {
+  int NT, KP, WS, QS;
+  __host__ __device__ static int ws_for(int KP) { return ((KP / 4) % 2 == 1) ? KP : KP + 4; }
+  __host__ __device__ GenShape(int nt, int K) : NT(nt), KP((K + 3) & ~3), WS(ws_for((K + 3) & ~3)), QS(2 * nt + 1) {}
+  __host__ __device__ size_t smem_floats() const { return size_t(NT) * KP + size_t(kGenChunk) * WS + size_t(kGenChunk) * QS; }
+};
+
+__global__ void __launch_bounds__(kGenThreads, 1) solve_generic_kernel(const SolveArgs a, int NT) {
+  if (*a.status || (a.halt && *a.halt)) return;
+  const int F = a.F, K = a.K;
+  const GenShape G(NT, K);
+  const int KP = G.KP, WS = G.WS, QS = G.QS;
+  extern __shared__ __align__(16) float smem[];
+  float* Hs = smem;                  // [NT][KP]
+  float* Wc = Hs + NT * KP;          // [chunk rows][WS]
+  float* QR = Wc + kGenChunk * WS;   // [chunk rows][q 0..NT-1 | r NT..2NT-1]
+  __shared__ const float* fptr[64];
+  __shared__ double red[kGenThreads / 32];
+  __shared__ double meanv[64];
+  __shared__ int s_bad;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n0 = blockIdx.x * NT;
+  const int nf = min(NT, a.nframes - n0);
+  if (tid < NT) {
+    const int64_t fr = tid < nf ? (a.vsel ? a.vsel[n0 + tid] : a.v0 + n0 + tid) : 0;
+    fptr[tid] = a.V + fr * a.ldv;
+  }
+  if (tid == 0) s_bad = 0;
+  __syncthreads();
+  if (a.h0_mode == 2) {
+    for (int n = warp; n < nf; n += kGenThreads / 32) {
+      double s = 0.0;
+      for (int f = lane; f < F; f += 32) s += double(fptr[n][f]);
+      s = warp_sum_d(s);
+      if (lane == 0) meanv[n] = s / double(F);
+    }
+    __syncthreads();
+  }
+  for (int idx = tid; idx < NT * KP; idx += kGenThreads) {
+    const int n = idx / KP, k = idx - n * KP;
+    float val = 0.0f;
+    if (n < nf && k < K) {
+      if (a.h0_mode == 0) {
+        val = a.H0[size_t(n0 + n) * K + k];
+      } else if (a.h0_mode == 1) {
+        const int64_t col = a.widx ? int64_t(a.widx[n0 + n]) : (a.wbase + n0 + n) % a.wmod;
+        const uint32_t tag = a.T[col];
+        val = float(double(a.U[size_t(col) * K + k]) * (a.P[size_t(a.c_now) * K + k] / a.P[size_t(tag) * K + k]));
+      } else {
+        const double mv = meanv[n] > a.epsd ? meanv[n] : a.epsd;
+        val = float(mv / a.kst->kmeanw * a.u01[size_t(n0 + n) * K + k]);
+      }
+      if (a.hscale) val = float(double(val) * a.hscale[k]);
+      if (a.check_h0 && !(val > 0.0f)) s_bad = 1;
+    }
+    Hs[idx] = val;
+  }
+  __syncthreads();
+  if (s_bad) {
+    if (tid == 0) atomicOr(a.status, ST_NONPOS_INIT);
+    return;
+  }
+  const float eps = a.eps;
+  const int npairs = K * NT;
+  float divacc = 0.0f;
+  const int passes = a.iters + (a.do_stats ? 1 : 0);
+  for (int pass = 0; pass < passes; ++pass) {
+    const bool stats_pass = pass == a.iters;
+    const bool want_div = a.div_first ? pass == 0 : stats_pass;
+    float num[kGenMaxPairs], den[kGenMaxPairs];
+#pragma unroll
+    for (int i = 0; i < kGenMaxPairs; ++i) num[i] = den[i] = 0.0f;
+    for (int c0 = 0; c0 < F; c0 += kGenChunk) {
+      const int rows = min(kGenChunk, F - c0);
+      __syncthreads();  // previous chunk's Wc / QR consumers are done
+      for (int i = tid; i < rows * WS / 4; i += kGenThreads)
+        reinterpret_cast<float4*>(Wc)[i] = __ldg(reinterpret_cast<const float4*>(a.W32 + size_t(c0) * WS) + i);
+      __syncthreads();
+      // phase A: lam, q, r for rows x NT cells
+      for (int cell = tid; cell < rows * NT; cell += kGenThreads) {
+        const int rl = cell / NT, n = cell - rl * NT;
+        const float* wr = Wc + rl * WS;
+        const float* hr = Hs + n * KP;
+        float acc = 0.0f;
+        for (int k = 0; k < KP; k += 4) {
+          const float4 w4 = *reinterpret_cast<const float4*>(wr + k);
+          const float4 h4 = *reinterpret_cast<const float4*>(hr + k);
+          acc = fmaf(w4.x, h4.x, acc);
+          acc = fmaf(w4.y, h4.y, acc);
+          acc = fmaf(w4.z, h4.z, acc);
+          acc = fmaf(w4.w, h4.w, acc);
+        }
+        const bool valid = n < nf;
+        const float v = valid ? __ldg(fptr[n] + c0 + rl) : 0.0f;
+        const float r = rcp_approx(acc + eps);
+        const float vpe = v + eps;
+        if (want_div && valid) divacc += is_term_ratio(vpe * r);
+        QR[rl * QS + n] = valid ? vpe * r * r : 0.0f;
+        QR[rl * QS + NT + n] = valid ? r : 0.0f;
+      }
+      __syncthreads();
+      if (!stats_pass) {
+        // phase B: num[k,n] += sum_f W[f,k] q[f,n], den with r
+#pragma unroll
+        for (int i = 0; i < kGenMaxPairs; ++i) {
+          const int p = tid + i * kGenThreads;
+          if (p < npairs) {
+            const int n = p / K, k = p - n * K;
+            float nu = num[i], de = den[i];
+            for (int rl = 0; rl < rows; ++rl) {
+              const float w = Wc[rl * WS + k];
+              nu = fmaf(w, QR[rl * QS + n], nu);
+              de = fmaf(w, QR[rl * QS + NT + n], de);
+            }
+            num[i] = nu;
+            den[i] = de;
+          }
+        }
+      } else if (a.stats) {
+        // statistics of the chunk rows: sa[f,k] = sum_n q h, sb[f,k] = sum_n r h
+        const int FP = (F + 3) & ~3;
+        float* outA = a.stats + size_t(blockIdx.x) * 2 * FP * KP;
+        float* outB = outA + size_t(FP) * KP;
+        for (int cell = tid; cell < rows * KP; cell += kGenThreads) {
+          const int k = cell / rows, rl = cell - k * rows;
+          float sa = 0.0f, sb = 0.0f;
+          for (int n = 0; n < nf; ++n) {
+            const float h = Hs[n * KP + k];
+            sa = fmaf(QR[rl * QS + n], h, sa);
+            sb = fmaf(QR[rl * QS + NT + n], h, sb);
+          }
+          outA[size_t(k) * FP + c0 + rl] = sa;
+          outB[size_t(k) * FP + c0 + rl] = sb;
+        }
+      }
+    }
+    if (!stats_pass) {
+      __syncthreads();  // all phase-A reads of Hs done
+#pragma unroll
+      for (int i = 0; i < kGenMaxPairs; ++i) {
+        const int p = tid + i * kGenThreads;
+        if (p < npairs) {
+          const int n = p / K, k = p - n * K;
+          if (n < nf) Hs[n * KP + k] *= sqrtf(num[i] / den[i]);
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (a.divpart) {
+    double d = warp_sum_d(double(divacc));
+    if (lane == 0) red[warp] = d;
+    __syncthreads();
+    if (tid == 0) {
+      double s = 0.0;
+      for (int w = 0; w < kGenThreads / 32; ++w) s += red[w];
+      a.divpart[blockIdx.x] = s;
+    }
+  }
+  __syncthreads();
+  if (a.Hout || a.write_store) {
+    for (int idx = tid; idx < nf * K; idx += kGenThreads) {
+      const int n = idx / K, k = idx - n * K;
+      const float h = Hs[n * KP + k];
+      if (a.Hout) a.Hout[size_t(n0 + n) * K + k] = h;
+      if (a.write_store) {
+        const int64_t col = a.widx ? int64_t(a.widx[n0 + n]) : (a.wbase + n0 + n) % a.wmod;
+        a.U[size_t(col) * K + k] = h;
+        if (k == 0) a.T[col] = a.c_now;
+      }
+    }
+  }
+}
+
+}  // namespace isnmf_dev

@@ -25,11 +25,12 @@ def rel(a, b):
     return float(np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-300)))
 
 
-def make_pair(F, K, beta, iters, N, restart="warm", seed=7, rho=1.0, a0=1e-3, v=None):
+def make_pair(F, K, beta, iters, N, restart="warm", seed=7, rho=1.0, a0=1e-3, v=None, generic=False):
     """Engine + oracle with the BASELINE initial state (A0 = B0 = a0, warm_h = 1)."""
     w0 = w_init(F, K, seed)
     v = spectrogram_np(F, K, N, seed=seed + 1) if v is None else v
-    eng = E.Online(F, K, beta, iters, restart=restart, seed=seed, n_store=N if restart == "warm" else 0)
+    eng = E.Online(F, K, beta, iters, restart=restart, seed=seed, n_store=N if restart == "warm" else 0,
+                   generic=generic)
     eng.set_dictionary(w0, np.full((F, K), a0), np.full((F, K), a0))
     eng.set_counters(0, 0, rho)
     orc = O.Online(w0, beta=beta, r=1.0, inner_iters=iters, restart=restart, seed=seed, dataset_size=N,
@@ -178,3 +179,32 @@ def test_errors_map_to_reference_types():
     with pytest.raises(E.EngineError) as e:
         eng.run(np.ones((F, 4), np.float32))
     assert e.value.kind == "NonPositiveInit"
+
+
+@pytest.mark.parametrize("F,K,beta,iters,N,restart", [
+    (1025, 256, 256, 8, 512, "warm"),   # config 4 shape (F, K, I), reduced beta / N for the fp64 oracle
+    (129, 80, 96, 4, 300, "fresh"),
+    (33, 3, 10, 5, 47, "warm"),
+])
+def test_generic_large_k_kernel(F, K, beta, iters, N, restart):
+    """The W-streaming generic kernel (K > 64 or forced) against the oracle."""
+    eng, orc, v = make_pair(F, K, beta, iters, N, restart=restart, rho=0.9, generic=True)
+    orc.run(v.astype(np.float64))
+    eng.run(v)
+    keys = ("w", "a", "b", "pending_a", "pending_b") + (("warm_h",) if restart == "warm" else ())
+    se, so = eng.state(warm_h=restart == "warm"), orc.state(warm_h=restart == "warm")
+    for k in keys:
+        assert rel(se[k], so[k]) < RTOL, (k, rel(se[k], so[k]))
+    assert se["commits"] == so["commits"] and se["pending_count"] == so["pending_count"]
+    assert rel(se["last_minibatch_obj"], so["last_minibatch_obj"]) < RTOL
+
+
+def test_generic_and_tiled_kernels_agree():
+    F, K, beta, iters, N = 257, 10, 100, 5, 1000
+    e1, _, v = make_pair(F, K, beta, iters, N)
+    e2, _, _ = make_pair(F, K, beta, iters, N, v=v, generic=True)
+    e1.run(v)
+    e2.run(v)
+    s1, s2 = e1.state(), e2.state()
+    for k in ("w", "a", "b"):
+        assert rel(s1[k], s2[k]) < 1e-5
