@@ -172,12 +172,13 @@ int isnmf_online_get_last_h(isnmf_online* ctx, double* h, int64_t n);
 int64_t isnmf_online_launch_count(isnmf_online* ctx);
 
 /* Profiling: between begin and end, CUDA events are recorded on the engine's
- * compute stream around every K1 (solve) launch.  end() waits for the stream
- * and returns the summed K1 device time, the K1 launch and frame counts, and
- * the device time of the whole region on that stream. */
+ * compute stream around every K1 (solve) launch and around each K2+K3
+ * (reduce + commit) pair.  end() waits for the stream and returns the summed K1
+ * device time, the K1 launch and frame counts, the device time of the whole
+ * region on that stream and the summed K2+K3 time. */
 int isnmf_online_profile_begin(isnmf_online* ctx);
 int isnmf_online_profile_end(isnmf_online* ctx, double* solve_ms, int64_t* solve_launches, int64_t* solve_frames,
-                             double* span_ms);
+                             double* span_ms, double* tail_ms);
 
 /* ---------------------------------------------------------------------------
  * Batch engine — batch_train (batch.hpp:84-143): per epoch one MM pass over H,

@@ -73,7 +73,7 @@ _SIGS = {
     "isnmf_host_alloc": ([I64], VP),
     "isnmf_host_free": ([VP], None),
     "isnmf_online_profile_begin": ([VP], C.c_int),
-    "isnmf_online_profile_end": ([VP, VP, VP, VP, VP], C.c_int),
+    "isnmf_online_profile_end": ([VP, VP, VP, VP, VP, VP], C.c_int),
     "isnmf_batch_train": ([VP, I64, I64, I64, I64, VP, VP, U64, D, D, VP, VP, VP, VP, VP, VP], C.c_int),
 }
 
@@ -285,10 +285,12 @@ class Profile:
         _check(lib().isnmf_online_profile_begin(self.o._h))
 
     def stop(self):
-        ms, nl, nf, span = D(), I64(), I64(), D()
-        _check(lib().isnmf_online_profile_end(self.o._h, C.byref(ms), C.byref(nl), C.byref(nf), C.byref(span)))
+        ms, nl, nf, span, tail = D(), I64(), I64(), D(), D()
+        _check(lib().isnmf_online_profile_end(self.o._h, C.byref(ms), C.byref(nl), C.byref(nf), C.byref(span),
+                                              C.byref(tail)))
         self._span = span.value
-        return dict(solve_ms=ms.value, solve_launches=nl.value, solve_frames=nf.value, span_ms=span.value)
+        return dict(solve_ms=ms.value, solve_launches=nl.value, solve_frames=nf.value, span_ms=span.value,
+                    tail_ms=tail.value)
 
     def span_ms(self):
         return self._span

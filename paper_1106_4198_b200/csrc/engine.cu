@@ -299,6 +299,8 @@ struct isnmf_online {
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
+  std::vector<cudaEvent_t> ev_tail;  // K2 start, K3 end per mini-batch (profiling)
+  size_t tail_used = 0;
   int64_t prof_frames = 0;
   cudaEvent_t ev_span[2] = {nullptr, nullptr};
   long long* phase_prof = nullptr;  // ISNMF_PHASE_PROF builds only
@@ -320,6 +322,7 @@ int online_free(isnmf_online* c) {
     if (c->ev_span[i]) cudaEventDestroy(c->ev_span[i]);
   }
   for (auto e : c->ev_pool) cudaEventDestroy(e);
+  for (auto e : c->ev_tail) cudaEventDestroy(e);
   if (c->cs) cudaStreamDestroy(c->cs);
   if (c->xs) cudaStreamDestroy(c->xs);
   delete c;
@@ -333,14 +336,16 @@ int read_state(isnmf_online* c, DevState* h) {
 }
 
 // Grows the P table (prefix products of column scales) to hold `rows` rows.
+// Stream-ordered (no host synchronisation), so growth never drains the queue.
 int ensure_P(isnmf_online* c, int64_t rows) {
   if (rows <= c->Pcap) return 0;
-  int64_t cap = std::max<int64_t>(rows, 2 * c->Pcap + 64);
+  const int64_t cap = std::max<int64_t>(rows, 2 * c->Pcap + 64);
   double* np = nullptr;
-  TRY(dalloc(&np, size_t(cap) * c->K));
-  CU(cudaStreamSynchronize(c->cs));
-  if (c->P) CU(cudaMemcpy(np, c->P, size_t(c->Pcap) * c->K * sizeof(double), cudaMemcpyDeviceToDevice));
-  dfree(c->P);
+  CU(cudaMallocAsync(reinterpret_cast<void**>(&np), size_t(cap) * c->K * sizeof(double), c->cs));
+  if (c->P) {
+    CU(cudaMemcpyAsync(np, c->P, size_t(c->Pcap) * c->K * sizeof(double), cudaMemcpyDeviceToDevice, c->cs));
+    CU(cudaFreeAsync(c->P, c->cs));
+  }
   c->P = np;
   c->Pcap = cap;
   return 0;
@@ -348,21 +353,20 @@ int ensure_P(isnmf_online* c, int64_t rows) {
 
 int ensure_trace(isnmf_online* c, int64_t n) {
   if (n <= c->tr_cap) return 0;
-  int64_t cap = std::max<int64_t>(n, 2 * c->tr_cap + 64);
+  const int64_t cap = std::max<int64_t>(n, 2 * c->tr_cap + 64);
   unsigned long long *t = nullptr, *ns = nullptr;
   double* o = nullptr;
-  TRY(dalloc(&t, cap));
-  TRY(dalloc(&ns, cap));
-  TRY(dalloc(&o, cap));
-  CU(cudaStreamSynchronize(c->cs));
+  CU(cudaMallocAsync(reinterpret_cast<void**>(&t), size_t(cap) * sizeof(*t), c->cs));
+  CU(cudaMallocAsync(reinterpret_cast<void**>(&ns), size_t(cap) * sizeof(*ns), c->cs));
+  CU(cudaMallocAsync(reinterpret_cast<void**>(&o), size_t(cap) * sizeof(*o), c->cs));
   if (c->tr_cap) {
-    CU(cudaMemcpy(t, c->tr_t, c->tr_cap * sizeof(*t), cudaMemcpyDeviceToDevice));
-    CU(cudaMemcpy(ns, c->tr_ns, c->tr_cap * sizeof(*ns), cudaMemcpyDeviceToDevice));
-    CU(cudaMemcpy(o, c->tr_obj, c->tr_cap * sizeof(*o), cudaMemcpyDeviceToDevice));
+    CU(cudaMemcpyAsync(t, c->tr_t, c->tr_cap * sizeof(*t), cudaMemcpyDeviceToDevice, c->cs));
+    CU(cudaMemcpyAsync(ns, c->tr_ns, c->tr_cap * sizeof(*ns), cudaMemcpyDeviceToDevice, c->cs));
+    CU(cudaMemcpyAsync(o, c->tr_obj, c->tr_cap * sizeof(*o), cudaMemcpyDeviceToDevice, c->cs));
+    CU(cudaFreeAsync(c->tr_t, c->cs));
+    CU(cudaFreeAsync(c->tr_ns, c->cs));
+    CU(cudaFreeAsync(c->tr_obj, c->cs));
   }
-  dfree(c->tr_t);
-  dfree(c->tr_ns);
-  dfree(c->tr_obj);
   c->tr_t = t;
   c->tr_ns = ns;
   c->tr_obj = o;
@@ -444,6 +448,14 @@ int launch_block(isnmf_online* c, const float* dv, int64_t ldv, int nb, const ui
   r.rho = c->rho;
   r.st = c->st;
   r.halt = &c->st->halt;
+  if (c->prof) {
+    while (c->ev_tail.size() < c->tail_used + 2) {
+      cudaEvent_t e;
+      CU(cudaEventCreate(&e));
+      c->ev_tail.push_back(e);
+    }
+    CU(cudaEventRecord(c->ev_tail[c->tail_used], c->cs));
+  }
   reduce_kernel<<<c->K * row_blocks(c->F), kRedThreads, 0, c->cs>>>(r);
   c->launches += 2;
   if (commit) {
@@ -470,6 +482,10 @@ int launch_block(isnmf_online* c, const float* dv, int64_t ldv, int nb, const ui
     commit_kernel<<<c->K * row_blocks(c->F), kCellsPerCta, 0, c->cs>>>(m);
     c->launches++;
     c->commits_host++;
+  }
+  if (c->prof) {
+    CU(cudaEventRecord(c->ev_tail[c->tail_used + 1], c->cs));
+    c->tail_used += 2;
   }
   c->t_host += uint64_t(nb);
   CU(cudaGetLastError());
@@ -969,13 +985,14 @@ int isnmf_online_profile_begin(isnmf_online* c) {
     if (!c->ev_span[i]) CU(cudaEventCreate(&c->ev_span[i]));
   c->prof = true;
   c->ev_used = 0;
+  c->tail_used = 0;
   c->prof_frames = 0;
   CU(cudaEventRecord(c->ev_span[0], c->cs));
   return 0;
 }
 
 int isnmf_online_profile_end(isnmf_online* c, double* solve_ms, int64_t* solve_launches, int64_t* solve_frames,
-                             double* span_ms) {
+                             double* span_ms, double* tail_ms) {
   if (!c || !c->prof) return fail(ISNMF_E_INVALID_ARG, "profile_end without profile_begin");
   CU(cudaEventRecord(c->ev_span[1], c->cs));
   CU(cudaEventSynchronize(c->ev_span[1]));
@@ -987,6 +1004,13 @@ int isnmf_online_profile_end(isnmf_online* c, double* solve_ms, int64_t* solve_l
   }
   float span = 0.0f;
   CU(cudaEventElapsedTime(&span, c->ev_span[0], c->ev_span[1]));
+  double tail = 0.0;
+  for (size_t i = 0; i + 1 < c->tail_used; i += 2) {
+    float ms = 0.0f;
+    CU(cudaEventElapsedTime(&ms, c->ev_tail[i], c->ev_tail[i + 1]));
+    tail += ms;
+  }
+  if (tail_ms) *tail_ms = tail;
   if (solve_ms) *solve_ms = tot;
   if (solve_launches) *solve_launches = int64_t(c->ev_used / 2);
   if (solve_frames) *solve_frames = c->prof_frames;

@@ -27,4 +27,5 @@ for rep in range(4):
     t2 = time.perf_counter()
     k = prof.stop()
     print(f"rep {rep}: enqueue {1e3*(t1-t0):.2f} ms, sync {1e3*(t2-t1):.2f} ms, span {k['span_ms']:.2f} ms, "
-          f"k1 {k['solve_ms']:.2f} ms / {k['solve_launches']} launches, frames/s {N/(k['span_ms']/1e3):.3e}")
+          f"k1 {k['solve_ms']:.2f} ms / {k['solve_launches']} launches, k2+k3 {k['tail_ms']:.2f} ms, "
+          f"frames/s {N/(k['span_ms']/1e3):.3e}")
