@@ -253,22 +253,43 @@ __device__ __forceinline__ void phase_a(const float* Ws, const float* Hs, float*
       for (int j = 0; j < TN; ++j) acc[i][j] = 0.0f;
     const float* wrow = Ws + (c0 + rg) * WS;
     const float* hrow = Hs + fg * TN * KP;
-#pragma unroll 1
-    for (int kc = 0; kc < KP / 4; ++kc) {
-      float4 w4[4];
+    // software-pipelined over k quads with ping-pong register sets: the 4 + TN
+    // float4 loads of quad kc+1 are in flight while the 16*TN FMAs of quad kc issue
+    constexpr int NQ = KP / 4;
+    float4 wa[4], ha[TN], wb[4], hb[TN];
+    auto load = [&](int kc, float4(&w4)[4], float4(&h4)[TN]) {
 #pragma unroll
       for (int i = 0; i < 4; ++i) w4[i] = *reinterpret_cast<const float4*>(wrow + 8 * i * WS + 4 * kc);
 #pragma unroll
-      for (int j = 0; j < TN; ++j) {
-        const float4 h4 = *reinterpret_cast<const float4*>(hrow + j * KP + 4 * kc);
+      for (int j = 0; j < TN; ++j) h4[j] = *reinterpret_cast<const float4*>(hrow + j * KP + 4 * kc);
+    };
+    // one k at a time across all 4*TN accumulators: consecutive FMAs are independent
+    auto fma4 = [&](const float4(&w4)[4], const float4(&h4)[TN]) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          acc[i][j] = fmaf(w4[i].x, h4.x, acc[i][j]);
-          acc[i][j] = fmaf(w4[i].y, h4.y, acc[i][j]);
-          acc[i][j] = fmaf(w4[i].z, h4.z, acc[i][j]);
-          acc[i][j] = fmaf(w4[i].w, h4.w, acc[i][j]);
-        }
-      }
+      for (int j = 0; j < TN; ++j)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[i][j] = fmaf(w4[i].x, h4[j].x, acc[i][j]);
+#pragma unroll
+      for (int j = 0; j < TN; ++j)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[i][j] = fmaf(w4[i].y, h4[j].y, acc[i][j]);
+#pragma unroll
+      for (int j = 0; j < TN; ++j)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[i][j] = fmaf(w4[i].z, h4[j].z, acc[i][j]);
+#pragma unroll
+      for (int j = 0; j < TN; ++j)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[i][j] = fmaf(w4[i].w, h4[j].w, acc[i][j]);
+    };
+    load(0, wa, ha);
+#pragma unroll 1
+    for (int kc = 0; kc < NQ; kc += 2) {
+      load(kc + 1 < NQ ? kc + 1 : kc, wb, hb);
+      fma4(wa, ha);
+      if (kc + 1 >= NQ) break;
+      load(kc + 2 < NQ ? kc + 2 : kc, wa, ha);
+      fma4(wb, hb);
     }
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -522,24 +543,37 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(const SolveArgs a) {
         for (int i = 0; i < 4; ++i)
 #pragma unroll
           for (int j = 0; j < TK; ++j) sa[i][j] = sb[i][j] = 0.0f;
-        const int islots = (rows + 7) / 8;
-#pragma unroll 1
-        for (int n = 0; n < nf; ++n) {
-          float hk[TK];
-          load_wk<TK>(Hs + n * KP, kgs, hk);
+        // pipelined over frames with ping-pong register sets: the loads of frame
+        // n+1 issue before the FMAs of frame n.  Rows past `rows` (tail chunk)
+        // accumulate stale staging values that are never stored.
+        const float* qr = QR + rgs * kQS;
+        float ha[TK], qa[4], ra[4], hb[TK], qb[4], rb[4];
+        auto load = [&](int n, float(&hk)[TK], float(&q)[4], float(&r)[4]) {
           const int off = (n / TN) * 8 + (n % TN);
+          load_wk<TK>(Hs + n * KP, kgs, hk);
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
-            if (i < islots) {
-              const float q = QR[(rgs + 8 * i) * kQS + off];
-              const float r = QR[(rgs + 8 * i) * kQS + kQR_R + off];
-#pragma unroll
-              for (int j = 0; j < TK; ++j) {
-                sa[i][j] = fmaf(q, hk[j], sa[i][j]);
-                sb[i][j] = fmaf(r, hk[j], sb[i][j]);
-              }
-            }
+            q[i] = qr[8 * i * kQS + off];
+            r[i] = qr[8 * i * kQS + kQR_R + off];
           }
+        };
+        auto fma_frame = [&](const float(&hk)[TK], const float(&q)[4], const float(&r)[4]) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < TK; ++j) {
+              sa[i][j] = fmaf(q[i], hk[j], sa[i][j]);
+              sb[i][j] = fmaf(r[i], hk[j], sb[i][j]);
+            }
+        };
+        load(0, ha, qa, ra);
+#pragma unroll 1
+        for (int n = 0; n < nf; n += 2) {
+          load(n + 1 < nf ? n + 1 : n, hb, qb, rb);
+          fma_frame(ha, qa, ra);
+          if (n + 1 >= nf) break;
+          load(n + 2 < nf ? n + 2 : n, ha, qa, ra);
+          fma_frame(hb, qb, rb);
         }
         const int FP = (F + 3) & ~3;  // partial planes padded so K2 can read float4 quads
         float* outA = a.stats + size_t(blockIdx.x) * 2 * FP * KP;
