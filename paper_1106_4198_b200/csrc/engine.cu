@@ -105,7 +105,21 @@ int smem_optin() {
 }
 
 int ws_for(int KP) { return ((KP / 4) % 2 == 1) ? KP : KP + 4; }
-int row_blocks(int F) { return (F + kCellsPerCta - 1) / kCellsPerCta; }
+bool fold_configured = false;
+
+// K2: one cluster of kFoldCluster CTAs per column of W.
+int launch_fold(const FoldArgs& f, cudaStream_t s) {
+  const size_t smem = fold_smem_bytes(f.F);
+  if (smem + 1024 > size_t(smem_optin()))
+    return fail(ISNMF_E_UNSUPPORTED, "F=%d too large for the commit kernel", f.F);
+  if (!fold_configured) {
+    CU(cudaFuncSetAttribute(fold_commit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin() - 1024));
+    fold_configured = true;
+  }
+  fold_commit_kernel<<<f.K * kFoldCluster, kFoldThreads, smem, s>>>(f);
+  return 0;
+}
+int fold_parts(int K) { return 2 * K * kFoldCluster; }
 int padded_f(int F) { return (F + 3) & ~3; }
 
 // Picks the variant for (F, K, frames per mini-batch).
@@ -270,8 +284,8 @@ struct isnmf_online {
   int WS = 0, KP = 0, NT = 0;
   cudaStream_t cs = nullptr, xs = nullptr;
   DevState* st = nullptr;
-  double *W64 = nullptr, *A = nullptr, *B = nullptr, *pa = nullptr, *pb = nullptr, *Wtmp = nullptr;
-  double* colpart = nullptr;
+  double *W64 = nullptr, *A = nullptr, *B = nullptr, *pa = nullptr, *pb = nullptr;
+  double* cta_part = nullptr;
   double* P = nullptr;
   int64_t Pcap = 0;
   float* W32 = nullptr;
@@ -312,7 +326,7 @@ int online_free(isnmf_online* c) {
   if (!c) return 0;
   if (c->cs) cudaStreamSynchronize(c->cs);
   if (c->xs) cudaStreamSynchronize(c->xs);
-  void* ptrs[] = {c->st, c->W64, c->A, c->B, c->pa, c->pb, c->Wtmp, c->colpart, c->P, c->W32, c->stats,
+  void* ptrs[] = {c->st, c->W64, c->A, c->B, c->pa, c->pb, c->cta_part, c->P, c->W32, c->stats,
                   c->divpart, c->U, c->T, c->u01, c->Hlast, c->tr_t, c->tr_obj, c->tr_ns, c->vbuf[0],
                   c->vbuf[1], c->ibuf[0], c->ibuf[1]};
   for (void* p : ptrs) dfree(p);
@@ -375,6 +389,32 @@ int ensure_trace(isnmf_online* c, int64_t n) {
 }
 
 // One block of nb frames inside a single mini-batch: K0? -> K1 -> K2 (-> K3).
+FoldArgs fold_args(const isnmf_online* c) {
+  FoldArgs r{};
+  r.stats = c->stats;
+  r.divpart = c->divpart;
+  r.F = c->F;
+  r.K = c->K;
+  r.KP = c->KP;
+  r.WS = c->WS;
+  r.W64 = c->W64;
+  r.pa = c->pa;
+  r.pb = c->pb;
+  r.A = c->A;
+  r.B = c->B;
+  r.W32 = c->W32;
+  r.P = c->P;
+  r.cta_part = c->cta_part;
+  r.rho = c->rho;
+  r.st = c->st;
+  r.halt = &c->st->halt;
+  r.tr_t = c->tr_t;
+  r.tr_obj = c->tr_obj;
+  r.tr_ns = c->tr_ns;
+  r.tr_cap = c->tr_cap;
+  return r;
+}
+
 int launch_block(isnmf_online* c, const float* dv, int64_t ldv, int nb, const uint64_t* widx_dev) {
   const int nblk = (nb + c->NT - 1) / c->NT;
   if (c->restart == ISNMF_RESTART_FRESH) {
@@ -428,26 +468,12 @@ int launch_block(isnmf_online* c, const float* dv, int64_t ldv, int nb, const ui
     c->prof_frames += nb;
   }
   const bool commit = (c->t_host + uint64_t(nb)) % uint64_t(c->beta) == 0;
-  ReduceArgs r{};
-  r.stats = c->stats;
-  r.divpart = c->divpart;
+  FoldArgs r = fold_args(c);
   r.nstat = nblk;
   r.ndiv = nblk;
-  r.colpart = c->colpart;
-  r.F = c->F;
-  r.K = c->K;
-  r.KP = c->KP;
   r.nframes = nb;
-  r.W64 = c->W64;
-  r.pa = c->pa;
-  r.pb = c->pb;
-  r.A = c->A;
-  r.B = c->B;
-  r.Wtmp = c->Wtmp;
   r.do_commit = commit;
-  r.rho = c->rho;
-  r.st = c->st;
-  r.halt = &c->st->halt;
+  r.eta = c->eta;
   if (c->prof) {
     while (c->ev_tail.size() < c->tail_used + 2) {
       cudaEvent_t e;
@@ -456,33 +482,9 @@ int launch_block(isnmf_online* c, const float* dv, int64_t ldv, int nb, const ui
     }
     CU(cudaEventRecord(c->ev_tail[c->tail_used], c->cs));
   }
-  reduce_kernel<<<c->K * row_blocks(c->F), kRedThreads, 0, c->cs>>>(r);
+  TRY(launch_fold(r, c->cs));
   c->launches += 2;
-  if (commit) {
-    CommitArgs m{};
-    m.F = c->F;
-    m.K = c->K;
-    m.WS = c->WS;
-    m.Wtmp = c->Wtmp;
-    m.W64 = c->W64;
-    m.A = c->A;
-    m.B = c->B;
-    m.W32 = c->W32;
-    m.P = c->P;
-    m.colpart = c->colpart;
-    m.cta_part = c->colpart + size_t(c->K) * row_blocks(c->F);
-    m.st = c->st;
-    m.halt = &c->st->halt;
-    m.eta = c->eta;
-    m.tr_t = c->tr_t;
-    m.tr_obj = c->tr_obj;
-    m.tr_ns = c->tr_ns;
-    m.tr_cap = c->tr_cap;
-    m.batch_mode = 0;
-    commit_kernel<<<c->K * row_blocks(c->F), kCellsPerCta, 0, c->cs>>>(m);
-    c->launches++;
-    c->commits_host++;
-  }
+  if (commit) c->commits_host++;
   if (c->prof) {
     CU(cudaEventRecord(c->ev_tail[c->tail_used + 1], c->cs));
     c->tail_used += 2;
@@ -653,7 +655,7 @@ int isnmf_online_create(isnmf_online** out, const isnmf_online_config* cfg) {
                      cudaGetErrorString(cudaGetLastError())));
   if ((rc = dalloc(&c->st, 1)) || (rc = dalloc(&c->W64, FK)) || (rc = dalloc(&c->A, FK)) ||
       (rc = dalloc(&c->B, FK)) || (rc = dalloc(&c->pa, FK)) || (rc = dalloc(&c->pb, FK)) ||
-      (rc = dalloc(&c->Wtmp, FK)) || (rc = dalloc(&c->colpart, 3 * size_t(c->K) * row_blocks(c->F))) ||
+      (rc = dalloc(&c->cta_part, size_t(fold_parts(c->K)))) ||
       (rc = dalloc(&c->W32, size_t(c->F) * c->WS)) ||
       (rc = dalloc(&c->stats, size_t(c->maxblk) * 2 * padded_f(c->F) * c->KP + 4)) ||
       (rc = dalloc(&c->divpart, c->maxblk)) ||
@@ -855,50 +857,16 @@ int isnmf_online_run(isnmf_online* c, const float* frames, int64_t ldv, int64_t 
 
 int isnmf_online_commit(isnmf_online* c) {
   if (!c) return fail(ISNMF_E_INVALID_ARG, "NULL context");
-  ReduceArgs r{};
-  r.stats = c->stats;
-  r.divpart = c->divpart;
-  r.nstat = 0;
-  r.ndiv = 0;
-  r.colpart = c->colpart;
-  r.F = c->F;
-  r.K = c->K;
-  r.KP = c->KP;
-  r.nframes = 0;
-  r.W64 = c->W64;
-  r.pa = c->pa;
-  r.pb = c->pb;
-  r.A = c->A;
-  r.B = c->B;
-  r.Wtmp = c->Wtmp;
-  r.do_commit = 1;
-  r.rho = c->rho;
-  r.st = c->st;
-  r.halt = &c->st->halt;
   TRY(ensure_P(c, int64_t(c->commits_host) + 2));
   TRY(ensure_trace(c, int64_t(c->commits_host - c->trace_base) + 2));
-  reduce_kernel<<<c->K * row_blocks(c->F), kRedThreads, 0, c->cs>>>(r);
-  CommitArgs m{};
-  m.F = c->F;
-  m.K = c->K;
-  m.WS = c->WS;
-  m.Wtmp = c->Wtmp;
-  m.W64 = c->W64;
-  m.A = c->A;
-  m.B = c->B;
-  m.W32 = c->W32;
-  m.P = c->P;
-  m.colpart = c->colpart;
-  m.cta_part = c->colpart + size_t(c->K) * row_blocks(c->F);
-  m.st = c->st;
-  m.halt = &c->st->halt;
-  m.eta = 0.0;
-  m.tr_t = c->tr_t;
-  m.tr_obj = c->tr_obj;
-  m.tr_ns = c->tr_ns;
-  m.tr_cap = c->tr_cap;
-  commit_kernel<<<c->K * row_blocks(c->F), kCellsPerCta, 0, c->cs>>>(m);
-  c->launches += 2;
+  FoldArgs r = fold_args(c);
+  r.nstat = 0;
+  r.ndiv = 0;
+  r.nframes = 0;
+  r.do_commit = 1;
+  r.eta = 0.0;
+  TRY(launch_fold(r, c->cs));
+  c->launches += 1;
   c->commits_host++;
   CU(cudaGetLastError());
   return online_finish(c, nullptr);
@@ -1087,7 +1055,7 @@ struct SolveWork {
   DevState* st = nullptr;
   float* W32 = nullptr;
   double* W64 = nullptr;
-  double *pa = nullptr, *pb = nullptr, *A = nullptr, *B = nullptr, *Wtmp = nullptr, *colpart = nullptr;
+  double *pa = nullptr, *pb = nullptr, *A = nullptr, *B = nullptr, *cta_part = nullptr;
   double *P = nullptr, *scale = nullptr;
   float* stats = nullptr;
   double* divpart = nullptr;
@@ -1095,7 +1063,7 @@ struct SolveWork {
 
   ~SolveWork() {
     if (s) cudaStreamSynchronize(s);
-    void* ptrs[] = {st, W32, W64, pa, pb, A, B, Wtmp, colpart, P, scale, stats, divpart, halt};
+    void* ptrs[] = {st, W32, W64, pa, pb, A, B, cta_part, P, scale, stats, divpart, halt};
     for (void* p : ptrs) dfree(p);
     if (s) cudaStreamDestroy(s);
   }
@@ -1117,8 +1085,7 @@ struct SolveWork {
     TRY(dalloc(&pb, FK));
     TRY(dalloc(&A, FK));
     TRY(dalloc(&B, FK));
-    TRY(dalloc(&Wtmp, FK));
-    TRY(dalloc(&colpart, 3 * size_t(K) * row_blocks(F)));
+    TRY(dalloc(&cta_part, size_t(fold_parts(K))));
     TRY(dalloc(&P, 2 * size_t(K)));
     TRY(dalloc(&scale, size_t(K)));
     TRY(dalloc(&stats, size_t(seg_blocks) * 2 * padded_f(F) * KP + 4));
@@ -1176,26 +1143,36 @@ struct SolveWork {
       a.status = &st->status;
       a.halt = halt;
       launch_solve(plan, nblk, a, s);
-      ReduceArgs r{};
-      r.stats = stats;
-      r.divpart = divpart;
+      FoldArgs r = fold_args();
       r.nstat = stats_on ? nblk : 0;
       r.ndiv = nblk;
-      r.colpart = colpart;
-      r.F = F;
-      r.K = K;
-      r.KP = KP;
       r.nframes = int(ns);
-      r.W64 = W64;
-      r.pa = pa;
-      r.pb = pb;
       r.do_commit = 0;
-      r.st = st;
-      r.halt = halt;
-      reduce_kernel<<<K * row_blocks(F), kRedThreads, 0, s>>>(r);
+      TRY(launch_fold(r, s));
       CU(cudaGetLastError());
     }
     return 0;
+  }
+
+  FoldArgs fold_args() const {
+    FoldArgs r{};
+    r.stats = stats;
+    r.divpart = divpart;
+    r.F = F;
+    r.K = K;
+    r.KP = KP;
+    r.WS = WS;
+    r.W64 = W64;
+    r.pa = pa;
+    r.pb = pb;
+    r.A = A;
+    r.B = B;
+    r.W32 = W32;
+    r.P = P;
+    r.cta_part = cta_part;
+    r.st = st;
+    r.halt = halt;
+    return r;
   }
 
   int state(DevState* h) {
@@ -1421,46 +1398,17 @@ int isnmf_batch_train(const float* v, int64_t ldv, int64_t F, int64_t N, int64_t
       CU(cudaMemcpy(wk.st, &h, sizeof(h), cudaMemcpyHostToDevice));
     }
     TRY(wk.pass(dv, dld, N, dh, 1, eps, dscale, true, true, false));
-    // elementwise commit with rho = 0: A = stats, B = stats, Wtmp = sqrt(A/B)
-    ReduceArgs r{};
-    r.stats = wk.stats;
-    r.divpart = wk.divpart;
+    // commit with rho = 0: A = stats, B = stats, W = sqrt(A/B), l1 rescale (scales -> dscale for H);
+    // P indexed by st->commits: commits stays 0 (2-row P)
+    FoldArgs r = wk.fold_args();
     r.nstat = 0;
     r.ndiv = 0;
-    r.colpart = wk.colpart;
-    r.F = int(F);
-    r.K = int(K);
-    r.KP = wk.KP;
     r.nframes = 0;
-    r.W64 = wk.W64;
-    r.pa = wk.pa;
-    r.pb = wk.pb;
-    r.A = wk.A;
-    r.B = wk.B;
-    r.Wtmp = wk.Wtmp;
     r.do_commit = 1;
     r.rho = 0.0;
-    r.st = wk.st;
-    r.halt = wk.halt;
-    reduce_kernel<<<int(K) * row_blocks(int(F)), kRedThreads, 0, wk.s>>>(r);
-    CommitArgs m{};
-    m.F = int(F);
-    m.K = int(K);
-    m.WS = wk.WS;
-    m.Wtmp = wk.Wtmp;
-    m.W64 = wk.W64;
-    m.A = wk.A;
-    m.B = wk.B;
-    m.W32 = wk.W32;
-    m.P = wk.P;
-    m.colpart = wk.colpart;
-    m.cta_part = wk.colpart + size_t(K) * row_blocks(int(F));
-    m.st = wk.st;
-    m.halt = wk.halt;
-    m.scale_out = dscale;
-    m.batch_mode = 1;
-    // commit_kernel indexes P by st->commits: keep commits at 0 (2-row P)
-    commit_kernel<<<int(K) * row_blocks(int(F)), kCellsPerCta, 0, wk.s>>>(m);
+    r.scale_out = dscale;
+    r.batch_mode = 1;
+    TRY(launch_fold(r, wk.s));
     CU(cudaGetLastError());
     DevState h{};
     TRY(wk.state(&h));

@@ -3,18 +3,17 @@
 // K1  solve_kernel   — fused mini-batch H solver (kernels.hpp:62-80) with the
 //                      statistics epilogue (kernels.hpp:95-108, online.hpp:360-361)
 //                      and the IS-divergence of the final fit (online.hpp:303-309).
-// K2  reduce_kernel  — deterministic fixed-order reduction of the per-CTA A/B
-//                      partials into pending (online.hpp:360-361) and the
-//                      elementwise half of dictionary_commit (online.hpp:319-325,
-//                      update_w kernels.hpp:142-159).
-// K3  commit_kernel  — per-column half of the commit: l1 renormalisation
-//                      (model.hpp:73-86), ||dW||_F (matrix.hpp:38-41), trace
-//                      point and eta stop rule (online.hpp:328-336, 390-396).
+// K2  fold_commit_kernel — deterministic fixed-order reduction of the per-CTA
+//                      A/B partials into pending (online.hpp:360-361) and, at a
+//                      mini-batch boundary, dictionary_commit (online.hpp:319-336:
+//                      update_w kernels.hpp:142-159, l1 renormalisation
+//                      model.hpp:73-86, ||dW||_F matrix.hpp:38-41, trace point,
+//                      eta stop rule online.hpp:390-396) in one cluster launch.
 // K0  fresh_kernel   — reference fresh-restart uniforms: std::mt19937_64 seeded
 //                      with splitmix64(mix_seed(seed, t)) (online.hpp:294-301,
 //                      rng.hpp:10-34), bit-exact.
 //
-// Layout in HBM: the fp64 state (W, A, B, pending, Wtmp) is column-major
+// Layout in HBM: the fp64 state (W, A, B, pending) is column-major
 // F x K like the reference's Eigen matrices (coalesced per-column commit);
 // per-CTA statistics partials are [2][KP][F] planes at the same cell offsets;
 // W32 is the solver's fp32 copy, row-major [F][WS] with zero pad columns.  See DESIGN.md for the roofline of each kernel.
@@ -55,8 +54,8 @@ struct DevState {
   double prev_obj;                   // batch: previous objective (batch.hpp:129)
   unsigned int status;               // error bits (ST_*)
   unsigned int halt;                 // eta stop rule fired
-  unsigned int ticket;               // last-block-done counter of commit_kernel
-  unsigned int pad;
+  unsigned int ticket;               // last-block-done counter of fold_commit_kernel
+  unsigned int pad;                  // error bits of the running fold_commit_kernel
 };
 
 // Optional per-phase cycle instrumentation (build with -DISNMF_PHASE_PROF):
@@ -627,139 +626,43 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(const SolveArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// K2 — reduce per-CTA partials into pending; commit part 1.
-// State arrays are column-major F x K (f fastest, the reference's Eigen
-// layout); cell c = k*F + f is also the offset inside each partial plane.
-// A CTA = (column k, 128-row block) = 32 row quads x 16 interleaved partial
-// groups; the group sums are combined in fixed order through shared memory.
+// K2 — fold_commit_kernel: the per-CTA statistics partials of one mini-batch
+// are folded into pending (online.hpp:360-361) and, at a mini-batch boundary,
+// the whole dictionary_commit (online.hpp:319-336) runs in the same launch:
+// A = rho A + pending, W = sqrt(A/B) (update_w, kernels.hpp:142-159), the l1
+// column rescale (model.hpp:73-86), ||dW||_F, the trace point and the eta stop.
+//
+// Grid = K columns x kFoldCluster CTAs; one thread-block cluster per column.
+// Rank r sums partial blocks [r*n/C, (r+1)*n/C) for every row of column k
+// (float4 loads, fp64 sums), the cluster exchanges the C row sums through
+// distributed shared memory and rank r finalises rows [r*F/C, (r+1)*F/C) —
+// the column sum s_k is exchanged the same way, so no second launch and no
+// global round trip is needed for the rescale.  Every sum is in a fixed order
+// (bitwise reproducible).  The last CTA of the grid (ticket) folds the
+// per-CTA ||dW||^2 / sum W partials in CTA order.
+//
+// Error bits found here go to DevState::fold_err and are merged into status by
+// the last CTA: status is read at kernel entry by every CTA, so it must not
+// change while a cluster is running (a CTA returning early would leave its
+// cluster waiting at the barrier).
 // ---------------------------------------------------------------------------
-struct ReduceArgs {
-  const float* stats;  // [nblk][2][KP][F]
+struct FoldArgs {
+  const float* stats;  // [nblk][2][KP][FP]
   const double* divpart;
   int nstat;  // statistics partial blocks to fold into pending (0: none)
   int ndiv;   // divergence partials to fold into pending_div
-  int F, K, KP;
+  int F, K, KP, WS;
   int nframes;
-  const double* W64;  // F x K column-major
-  double* pa;         // pending_a
+  double* W64;  // F x K column-major
+  double* pa;   // pending_a
   double* pb;
   double* A;
   double* B;
-  double* Wtmp;
-  double* colpart;  // [gridDim]: this CTA's fixed-order sum of W_tmp over its rows of column k
+  float* W32;
+  double* P;         // prefix products of the column scales [commits+1][K]
+  double* cta_part;  // [gridDim][2]: dW^2, sum W of this CTA
   int do_commit;
   double rho;
-  DevState* st;
-  const unsigned int* halt;
-};
-
-constexpr int kRedGroups = 16;                 // interleaved partial groups per cell quad
-constexpr int kRedThreads = 32 * kRedGroups;   // 512
-constexpr int kCellsPerCta = 128;              // 32 quads x 4 cells
-
-__global__ void __launch_bounds__(kRedThreads) reduce_kernel(const ReduceArgs a) {
-  if (a.st->status || *a.halt) return;
-  __shared__ double red[kRedGroups][32][8];
-  __shared__ double csum[32];
-  const int q = threadIdx.x & 31, g = threadIdx.x >> 5;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    double d = 0.0;
-    for (int b = 0; b < a.ndiv; ++b) d += a.divpart[b];
-    a.st->pending_div += d;
-    a.st->pending_count += (unsigned long long)a.nframes;
-    a.st->t += (unsigned long long)a.nframes;
-  }
-  // CTA = (column k, block of 128 rows); quad q = rows f0 .. f0+3
-  const int nrb = (a.F + kCellsPerCta - 1) / kCellsPerCta;
-  const int k = blockIdx.x / nrb, rb = blockIdx.x - k * nrb;
-  const int f0 = rb * kCellsPerCta + q * 4;
-  const int FP = (a.F + 3) & ~3;
-  const size_t plane = size_t(FP) * a.KP;
-  double sa[4] = {0.0, 0.0, 0.0, 0.0}, sb[4] = {0.0, 0.0, 0.0, 0.0};
-  if (f0 < a.F) {
-    const float* base = a.stats + size_t(k) * FP + f0;
-#pragma unroll 4
-    for (int b = g; b < a.nstat; b += kRedGroups) {
-      const float4 x = __ldcg(reinterpret_cast<const float4*>(base + size_t(b) * 2 * plane));
-      const float4 y = __ldcg(reinterpret_cast<const float4*>(base + size_t(b) * 2 * plane + plane));
-      sa[0] += x.x;
-      sa[1] += x.y;
-      sa[2] += x.z;
-      sa[3] += x.w;
-      sb[0] += y.x;
-      sb[1] += y.y;
-      sb[2] += y.z;
-      sb[3] += y.w;
-    }
-  }
-#pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    red[g][q][e] = sa[e];
-    red[g][q][4 + e] = sb[e];
-  }
-  __syncthreads();
-  if (g == 0) {
-    double cs = 0.0;
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      double ta = 0.0, tb = 0.0;
-#pragma unroll
-      for (int gg = 0; gg < kRedGroups; ++gg) {
-        ta += red[gg][q][e];
-        tb += red[gg][q][4 + e];
-      }
-      if (f0 + e >= a.F) break;
-      const int cell = k * a.F + f0 + e;
-      const double w = a.W64[cell];
-      const double pa = a.pa[cell] + w * w * ta;
-      const double pb = a.pb[cell] + tb;
-      if (!a.do_commit) {
-        a.pa[cell] = pa;
-        a.pb[cell] = pb;
-        continue;
-      }
-      const double An = a.rho * a.A[cell] + pa;  // rho scales the past (online.hpp:319-320)
-      const double Bn = a.rho * a.B[cell] + pb;
-      a.A[cell] = An;
-      a.B[cell] = Bn;
-      a.pa[cell] = 0.0;
-      a.pb[cell] = 0.0;
-      double wn = w;
-      if (Bn > 0.0)
-        wn = sqrt(An / Bn);
-      else if (An > 0.0)
-        atomicOr(&a.st->status, ST_INCONSISTENT);
-      if (!isfinite(wn)) atomicOr(&a.st->status, ST_NONFINITE_W);
-      a.Wtmp[cell] = wn;
-      cs += wn;
-    }
-    if (a.do_commit) csum[q] = cs;
-  }
-  if (!a.do_commit) return;
-  __syncthreads();
-  if (threadIdx.x == 0) {  // fixed-order partial sum of W_tmp over this CTA's rows of column k
-    double c = 0.0;
-    for (int i = 0; i < 32; ++i) c += csum[i];
-    a.colpart[blockIdx.x] = c;
-  }
-}
-
-// ---------------------------------------------------------------------------
-// K3 — column renormalisation, ||dW||_F, trace point, stop rule.  Same tiling
-// as K2: a CTA scales its 128 rows of column k by s_k (the K2 row-block
-// partials of column k in fixed order, identical in every CTA), and the last
-// CTA to finish folds the per-CTA ||dW||^2 and sum W in CTA order.
-// ---------------------------------------------------------------------------
-struct CommitArgs {
-  int F, K, WS;
-  const double* colpart;   // [K * nrb] from K2
-  double* cta_part;        // [gridDim][2]: dW^2, sum W of this CTA
-  const double* Wtmp;
-  double* W64;
-  double* A;
-  double* B;
-  float* W32;
-  double* P;  // prefix products of the column scales [commits+1][K]
   DevState* st;
   unsigned int* halt;
   double eta;
@@ -771,108 +674,242 @@ struct CommitArgs {
   int batch_mode;
 };
 
+constexpr int kFoldCluster = 4;
+constexpr int kFoldThreads = 512;
+constexpr int kFoldWarps = kFoldThreads / 32;
+
+__host__ __device__ inline int fold_groups(int F) {
+  const int nq = (F + 3) / 4;
+  const int g = kFoldThreads / nq;
+  return g < 1 ? 1 : (g > 16 ? 16 : g);
+}
+// dynamic shared memory of fold_commit_kernel: row sums [2][F], W_tmp [F], group partials
+__host__ __device__ inline size_t fold_smem_bytes(int F) {
+  const int nq = (F + 3) / 4, g = fold_groups(F);
+  return sizeof(double) * (3 * size_t(F) + (g > 1 ? size_t(g) * nq * 8 : 0));
+}
+
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
 
-// s_k: the K2 row-block partials of column k summed in row-block order.
-__device__ __forceinline__ double column_scale(const double* colpart, int nrb, int k) {
+__device__ __forceinline__ unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// generic address of `p` (this CTA's shared memory) in the shared memory of cluster rank `r`
+template <class T>
+__device__ __forceinline__ const T* map_rank(const T* p, unsigned r) {
+  const T* q;
+  asm volatile("mapa.u64 %0, %1, %2;" : "=l"(q) : "l"(p), "r"(r));
+  return q;
+}
+
+// fixed-order block sum (warp tree, then warps in order); valid in thread 0
+__device__ __forceinline__ double block_sum_d(double v, double* red) {
+  v = warp_sum_d(v);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
   double s = 0.0;
-  for (int rb = 0; rb < nrb; ++rb) s += colpart[k * nrb + rb];
+  if (threadIdx.x == 0)
+    for (int w = 0; w < kFoldWarps; ++w) s += red[w];
   return s;
 }
 
-__global__ void __launch_bounds__(kCellsPerCta) commit_kernel(const CommitArgs a) {
-  if (a.st->status || *a.halt) return;
-  __shared__ double sh_d[kCellsPerCta / 32], sh_w[kCellsPerCta / 32];
-  __shared__ int s_bad, s_last;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nrb = (a.F + kCellsPerCta - 1) / kCellsPerCta;
-  const int k = blockIdx.x / nrb, f = (blockIdx.x - k * nrb) * kCellsPerCta + tid;
-  const int cell = k * a.F + f;
-  if (tid == 0) s_bad = 0;
-  __syncthreads();
-  double d2 = 0.0, cw = 0.0;
-  if (f < a.F) {
-    const double sc = column_scale(a.colpart, nrb, k);
-    if (!(sc > 0.0)) {
-      s_bad = 1;
+__global__ void __cluster_dims__(kFoldCluster, 1, 1) __launch_bounds__(kFoldThreads)
+    fold_commit_kernel(const FoldArgs a) {
+  if (a.st->status || *a.halt) return;  // both fixed for the whole launch (see above)
+  extern __shared__ __align__(16) double fsm[];
+  __shared__ double red[kFoldWarps];
+  __shared__ double s_cs, s_sc;
+  __shared__ int s_last;
+  const int F = a.F, tid = threadIdx.x;
+  const unsigned r = cluster_rank();
+  const int k = blockIdx.x / kFoldCluster;
+  double* sums = fsm;           // [2][F]: this rank's partial sums of column k
+  double* wt = fsm + 2 * F;     // [F]: W_tmp of this rank's rows
+  double* grp = fsm + 3 * F;    // [G][NQ][8]
+  if (blockIdx.x == 0 && tid < 32) {  // divergence + counters (fixed order: lane-strided, then the warp tree)
+    double d = 0.0;
+    for (int b = tid; b < a.ndiv; b += 32) d += a.divpart[b];
+    d = warp_sum_d(d);
+    if (tid == 0) {
+      a.st->pending_div += d;
+      a.st->pending_count += (unsigned long long)a.nframes;
+      a.st->t += (unsigned long long)a.nframes;
+    }
+  }
+  // ---- 1. this rank's share of the partial blocks, all rows of column k
+  const int NQ = (F + 3) / 4, G = fold_groups(F);
+  const int FP = (F + 3) & ~3;
+  const size_t plane = size_t(FP) * a.KP;
+  const int b0 = int((long long)r * a.nstat / kFoldCluster), b1 = int((long long)(r + 1) * a.nstat / kFoldCluster);
+  for (int it = tid; it < NQ * G; it += kFoldThreads) {
+    const int q = it % NQ, g = it / NQ;
+    const float* base = a.stats + size_t(k) * FP + 4 * q;
+    double s[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll 4
+    for (int b = b0 + g; b < b1; b += G) {
+      const float4 x = __ldcg(reinterpret_cast<const float4*>(base + size_t(b) * 2 * plane));
+      const float4 y = __ldcg(reinterpret_cast<const float4*>(base + size_t(b) * 2 * plane + plane));
+      s[0] += x.x;
+      s[1] += x.y;
+      s[2] += x.z;
+      s[3] += x.w;
+      s[4] += y.x;
+      s[5] += y.y;
+      s[6] += y.z;
+      s[7] += y.w;
+    }
+    if (G == 1) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (4 * q + e < F) {
+          sums[4 * q + e] = s[e];
+          sums[F + 4 * q + e] = s[4 + e];
+        }
     } else {
-      const double wn = a.Wtmp[cell] / sc;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) grp[size_t(it) * 8 + e] = s[e];
+    }
+  }
+  if (G > 1) {
+    __syncthreads();
+    for (int f = tid; f < F; f += kFoldThreads) {
+      const int q = f >> 2, e = f & 3;
+      double ta = 0.0, tb = 0.0;
+      for (int g = 0; g < G; ++g) {
+        ta += grp[(size_t(g) * NQ + q) * 8 + e];
+        tb += grp[(size_t(g) * NQ + q) * 8 + 4 + e];
+      }
+      sums[f] = ta;
+      sums[F + f] = tb;
+    }
+  }
+  cluster_sync_all();
+  // ---- 2. rows [lo, hi) of column k: cluster-wide sums in rank order, pending / commit part 1
+  const int lo = int((long long)r * F / kFoldCluster), hi = int((long long)(r + 1) * F / kFoldCluster);
+  double cs = 0.0;
+  unsigned bad = 0;
+  for (int f = lo + tid; f < hi; f += kFoldThreads) {
+    double ta = 0.0, tb = 0.0;
+#pragma unroll
+    for (int i = 0; i < kFoldCluster; ++i) {
+      const double* rs = map_rank(sums, unsigned(i));
+      ta += rs[f];
+      tb += rs[F + f];
+    }
+    const size_t cell = size_t(k) * F + f;
+    const double w = a.W64[cell];
+    const double pa = a.pa[cell] + w * w * ta;
+    const double pb = a.pb[cell] + tb;
+    if (!a.do_commit) {
+      a.pa[cell] = pa;
+      a.pb[cell] = pb;
+      continue;
+    }
+    const double An = a.rho * a.A[cell] + pa;  // rho scales the past (online.hpp:319-320)
+    const double Bn = a.rho * a.B[cell] + pb;
+    a.A[cell] = An;
+    a.B[cell] = Bn;
+    a.pa[cell] = 0.0;
+    a.pb[cell] = 0.0;
+    double wn = w;
+    if (Bn > 0.0)
+      wn = sqrt(An / Bn);
+    else if (An > 0.0)
+      bad |= ST_INCONSISTENT;
+    if (!isfinite(wn)) bad |= ST_NONFINITE_W;
+    wt[f] = wn;
+    cs += wn;
+  }
+  if (!a.do_commit) {
+    cluster_sync_all();  // the other ranks may still read this CTA's sums
+    return;
+  }
+  if (bad) atomicOr(&a.st->pad, bad);
+  cs = block_sum_d(cs, red);
+  if (tid == 0) s_cs = cs;
+  cluster_sync_all();
+  // ---- 3. column scale s_k (rank order), rescale of this rank's rows
+  if (tid == 0) {
+    double sc = 0.0;
+    for (int i = 0; i < kFoldCluster; ++i) sc += *map_rank(&s_cs, unsigned(i));
+    s_sc = sc;
+  }
+  cluster_sync_all();  // s_sc visible; no rank reads another's shared memory after this
+  const double sc = s_sc;
+  double d2 = 0.0, cw = 0.0;
+  if (!(sc > 0.0)) {
+    if (tid == 0) atomicOr(&a.st->pad, ST_ZERO_COLUMN);
+  } else {
+    for (int f = lo + tid; f < hi; f += kFoldThreads) {
+      const size_t cell = size_t(k) * F + f;
+      const double wn = wt[f] / sc;
       const double d = wn - a.W64[cell];
-      d2 = d * d;
-      cw = wn;
+      d2 += d * d;
+      cw += wn;
       a.W64[cell] = wn;
       a.A[cell] /= sc;
       a.B[cell] *= sc;
       a.W32[size_t(f) * a.WS + k] = float(wn);
-      if (f == 0) {
-        const unsigned long long c = a.st->commits;
-        a.P[size_t(c + 1) * a.K + k] = a.P[size_t(c) * a.K + k] * sc;
-        if (a.scale_out) a.scale_out[k] = sc;
-      }
+    }
+    if (r == 0 && tid == 0) {
+      const unsigned long long c = a.st->commits;
+      a.P[size_t(c + 1) * a.K + k] = a.P[size_t(c) * a.K + k] * sc;
+      if (a.scale_out) a.scale_out[k] = sc;
     }
   }
-  d2 = warp_sum_d(d2);
-  cw = warp_sum_d(cw);
-  if (lane == 0) {
-    sh_d[warp] = d2;
-    sh_w[warp] = cw;
-  }
-  __syncthreads();
+  d2 = block_sum_d(d2, red);
+  cw = block_sum_d(cw, red);
   if (tid == 0) {
-    if (s_bad) atomicOr(&a.st->status, ST_ZERO_COLUMN);
-    double dd = 0.0, ww = 0.0;
-    for (int w = 0; w < kCellsPerCta / 32; ++w) {
-      dd += sh_d[w];
-      ww += sh_w[w];
-    }
-    a.cta_part[2 * blockIdx.x] = dd;
-    a.cta_part[2 * blockIdx.x + 1] = ww;
+    a.cta_part[2 * blockIdx.x] = d2;
+    a.cta_part[2 * blockIdx.x + 1] = cw;
     __threadfence();
     s_last = atomicAdd(&a.st->ticket, 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  if (s_last) {  // last CTA: fold the per-CTA partials (fixed order: strided per thread, then by warp)
-    __threadfence();
-    double pd = 0.0, pw = 0.0;
-    for (unsigned int b = tid; b < gridDim.x; b += kCellsPerCta) {
-      pd += __ldcg(a.cta_part + 2 * b);
-      pw += __ldcg(a.cta_part + 2 * b + 1);
+  if (!s_last) return;
+  // ---- 4. last CTA: ||dW||_F, mean W, objective, trace point, stop rule
+  __threadfence();
+  double pd = 0.0, pw = 0.0;
+  for (unsigned int b = tid; b < gridDim.x; b += kFoldThreads) {
+    pd += __ldcg(a.cta_part + 2 * b);
+    pw += __ldcg(a.cta_part + 2 * b + 1);
+  }
+  pd = block_sum_d(pd, red);
+  pw = block_sum_d(pw, red);
+  if (tid == 0) {
+    DevState* st = a.st;
+    st->ticket = 0;
+    const unsigned int err = *reinterpret_cast<volatile unsigned int*>(&st->pad);
+    st->pad = 0;
+    if (err) {
+      st->status |= err;
+      return;
     }
-    pd = warp_sum_d(pd);
-    pw = warp_sum_d(pw);
-    __syncthreads();
-    if (lane == 0) {
-      sh_d[warp] = pd;
-      sh_w[warp] = pw;
+    const unsigned long long c = st->commits;
+    st->last_delta = sqrt(pd);
+    st->kmeanw = double(a.K) * (pw / (double(a.F) * double(a.K)));
+    st->last_obj = st->pending_count ? st->pending_div / double(st->pending_count) : 0.0;
+    const long long ti = (long long)(c - st->trace_base);
+    if (a.tr_t && ti >= 0 && ti < a.tr_cap) {
+      a.tr_t[ti] = st->t;
+      a.tr_obj[ti] = st->last_obj;
+      a.tr_ns[ti] = globaltimer_ns();
     }
-    __syncthreads();
-    if (tid == 0) {
-      double sd = 0.0, sw = 0.0;
-      for (int w = 0; w < kCellsPerCta / 32; ++w) {
-        sd += sh_d[w];
-        sw += sh_w[w];
-      }
-      DevState* st = a.st;
-      const unsigned long long c = st->commits;
-      st->last_delta = sqrt(sd);
-      st->kmeanw = double(a.K) * (sw / (double(a.F) * double(a.K)));
-      st->last_obj = st->pending_count ? st->pending_div / double(st->pending_count) : 0.0;
-      const long long ti = (long long)(c - st->trace_base);
-      if (a.tr_t && ti >= 0 && ti < a.tr_cap) {
-        a.tr_t[ti] = st->t;
-        a.tr_obj[ti] = st->last_obj;
-        a.tr_ns[ti] = globaltimer_ns();
-      }
-      st->pending_div = 0.0;
-      st->pending_count = 0;
-      st->commits = c + 1;
-      st->ticket = 0;
-      if (!a.batch_mode && a.eta > 0.0 && st->last_delta < a.eta) *a.halt = 1u;
-    }
+    st->pending_div = 0.0;
+    st->pending_count = 0;
+    st->commits = c + 1;
+    if (!a.batch_mode && a.eta > 0.0 && st->last_delta < a.eta) *a.halt = 1u;
   }
 }
 
