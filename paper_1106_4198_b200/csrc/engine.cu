@@ -318,6 +318,7 @@ struct isnmf_online {
   int64_t prof_frames = 0;
   cudaEvent_t ev_span[2] = {nullptr, nullptr};
   long long* phase_prof = nullptr;  // ISNMF_PHASE_PROF builds only
+  long long* fold_prof = nullptr;   // ISNMF_PHASE_PROF builds only
 };
 
 namespace {
@@ -412,6 +413,7 @@ FoldArgs fold_args(const isnmf_online* c) {
   r.tr_obj = c->tr_obj;
   r.tr_ns = c->tr_ns;
   r.tr_cap = c->tr_cap;
+  r.tprof = c->fold_prof;
   return r;
 }
 
@@ -943,6 +945,19 @@ int isnmf_debug_phase_prof(isnmf_online* c, long long* out, int64_t cap, int32_t
   if (out) CU(cudaMemcpy(out, c->phase_prof, std::min<size_t>(n, size_t(cap)) * sizeof(long long),
                          cudaMemcpyDeviceToHost));
   if (reset) CU(cudaMemset(c->phase_prof, 0, n * sizeof(long long)));
+  return 0;
+}
+
+// per-CTA globaltimer stamps of the last fold_commit_kernel launch: [K*kFoldCluster][8]
+int isnmf_debug_fold_prof(isnmf_online* c, long long* out, int64_t cap) {
+  const size_t n = size_t(c->K) * kFoldCluster * 8;
+  if (!c->fold_prof) {
+    CU(cudaMalloc(&c->fold_prof, n * sizeof(long long)));
+    CU(cudaMemset(c->fold_prof, 0, n * sizeof(long long)));
+  }
+  CU(cudaStreamSynchronize(c->cs));
+  if (out) CU(cudaMemcpy(out, c->fold_prof, std::min<size_t>(n, size_t(cap)) * sizeof(long long),
+                         cudaMemcpyDeviceToHost));
   return 0;
 }
 #endif

@@ -221,14 +221,23 @@ __device__ __forceinline__ void load_x(const float* xr, float (&x)[TN]) {
   }
 }
 
-// Phase A of one warp chunk: lam = W h + eps for `rows` rows x NT frames;
-// q = (v+eps)/lam^2 and r = 1/lam are staged into the warp's Q/R rows
-// ([row][nd][ng][8], padding lanes of invalid frames hold 0).
-// V values of a full chunk for this lane's phase-A cells (rows rg+8i, frames
-// fg*TN+j), issued one chunk ahead so the L2 latency hides behind phase B.
+// Lane -> role maps.  An LDS.128 costs 2 shared-memory wavefronts when every
+// aligned lane quad reads at most 2 distinct 16-byte addresses and 4 otherwise
+// (measured, tools/probe/lds_probe.cu), so each quad spans 2 values of each of
+// the two operand indices: phase A (row group rg 0..7, frame group fg 0..3)
+// and phase B (k group kg 0..3, frame group ng 0..3, nd = num/den).
+__device__ __forceinline__ int pa_rg(int lane) { return ((lane >> 1) & 1) | (((lane >> 2) & 3) << 1); }
+__device__ __forceinline__ int pa_fg(int lane) { return (lane & 1) | (((lane >> 4) & 1) << 1); }
+__device__ __forceinline__ int pb_kg(int lane) { return (lane & 1) | (((lane >> 2) & 1) << 1); }
+__device__ __forceinline__ int pb_ng(int lane) { return ((lane >> 1) & 1) | (((lane >> 3) & 1) << 1); }
+__device__ __forceinline__ int pb_lane(int kg, int ng, int nd) {
+  return (kg & 1) | ((ng & 1) << 1) | ((kg >> 1) << 2) | ((ng >> 1) << 3) | (nd << 4);
+}
+
+// V values of a full chunk for this lane's phase-A cells (rows rg+8i, frames fg*TN+j).
 template <int TN>
 __device__ __forceinline__ void load_v(float (&vv)[4][TN], const float* const* fptr, int c0, int nf, int lane) {
-  const int rg = lane & 7, fg = lane >> 3;
+  const int rg = pa_rg(lane), fg = pa_fg(lane);
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -238,13 +247,21 @@ __device__ __forceinline__ void load_v(float (&vv)[4][TN], const float* const* f
     }
 }
 
+// Phase A of one warp chunk: lam = W h + eps for `rows` rows x NT frames;
+// q = (v+eps)/lam^2 and r = 1/lam are staged into the warp's Q/R rows
+// ([row][nd][ng][8], padding lanes of invalid frames hold 0).  For a full
+// chunk vv holds the V values of this lane's cells (rows rg+8i, frames
+// fg*TN+j), loaded one chunk ahead by load_v so the L2 latency hides behind
+// phase B; a tail chunk (rows < 32) takes one (row, frame) cell per lane and
+// vt = V of cell `lane` when rows * NT <= 32 (loaded once per launch).
 template <int TK, int TN>
 __device__ __forceinline__ void phase_a(const float* Ws, const float* Hs, float* QR, const float* const* fptr,
-                                        int c0, int rows, int nf, float eps, int lane, const float (&vv)[4][TN]) {
+                                        int c0, int rows, int nf, float eps, int lane, const float (&vv)[4][TN],
+                                        float vt) {
   using S = SolveShape<TK, TN>;
   constexpr int KP = S::KP, NT = S::NT, WS = S::WS;
   if (rows == kChunk) {
-    const int rg = lane & 7, fg = lane >> 3;  // 8 row groups x 4 frame groups
+    const int rg = pa_rg(lane), fg = pa_fg(lane);  // 8 row groups x 4 frame groups
     float acc[4][TN];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
@@ -303,13 +320,14 @@ __device__ __forceinline__ void phase_a(const float* Ws, const float* Hs, float*
       }
     }
   } else {
-    // tail rows (F not a multiple of 32 per warp): one (row, frame) cell per lane
+    // tail rows (F not a multiple of 32 per warp): one (row, frame) cell per lane,
+    // the k loop unrolled so every load is in flight before the FMA chain
     for (int cell = lane; cell < rows * NT; cell += 32) {
       const int rl = cell / NT, n = cell - rl * NT;
       const float* wr = Ws + (c0 + rl) * WS;
       const float* hr = Hs + n * KP;
       float acc = 0.0f;
-#pragma unroll 1
+#pragma unroll
       for (int kc = 0; kc < KP / 4; ++kc) {
         const float4 w4 = *reinterpret_cast<const float4*>(wr + 4 * kc);
         const float4 h4 = *reinterpret_cast<const float4*>(hr + 4 * kc);
@@ -319,7 +337,7 @@ __device__ __forceinline__ void phase_a(const float* Ws, const float* Hs, float*
         acc = fmaf(w4.w, h4.w, acc);
       }
       const bool valid = n < nf;
-      const float v = valid ? __ldg(fptr[n] + c0 + rl) : 0.0f;
+      const float v = !valid ? 0.0f : (rows * NT <= 32 ? vt : __ldg(fptr[n] + c0 + rl));
       const float r = rcp_approx(acc + eps);
       const float q = (v + eps) * r * r;
       float* qrow = QR + rl * kQS + (n / TN) * 8 + (n % TN);
@@ -447,11 +465,20 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(const SolveArgs a) {
   auto next_full = [&](int c0) { return (c0 + kChunk < r0 + nfull * kChunk) ? c0 + kChunk : r0; };
   float vv[4][TN];
   if (nfull > 0) load_v<TN>(vv, fptr, r0, nf, lane);
+  // V of the tail chunk's cell `lane` (constant over the passes)
+  float vt = 0.0f;
+  {
+    const int tr = r1 - r0 - nfull * kChunk;
+    if (tr > 0 && tr * NT <= 32 && lane < tr * NT) {
+      const int rl = lane / NT, n = lane - rl * NT;
+      if (n < nf) vt = __ldg(fptr[n] + r0 + nfull * kChunk + rl);
+    }
+  }
   float* QR = UN + warp * (kChunk * kQS);
   const float eps = a.eps;
   float divacc = 0.0f;
   // phase-B lane roles: 4 k groups x 4 frame groups x {num, den}
-  const int kg = lane & 3, ng = (lane >> 2) & 3, nd = lane >> 4;
+  const int kg = pb_kg(lane), ng = pb_ng(lane), nd = lane >> 4;
 
   for (int pass = 0; pass < a.iters; ++pass) {
     float accB[TK][TN];
@@ -462,7 +489,7 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(const SolveArgs a) {
 
     for (int c0 = r0; c0 < r1; c0 += kChunk) {
       const int rows = min(kChunk, r1 - c0);
-      phase_a<TK, TN>(Ws, Hs, QR, fptr, c0, rows, nf, eps, lane, vv);
+      phase_a<TK, TN>(Ws, Hs, QR, fptr, c0, rows, nf, eps, lane, vv, vt);
       if (rows == kChunk) load_v<TN>(vv, fptr, next_full(c0), nf, lane);
       __syncwarp();
       if (a.div_first && pass == 0) divacc += chunk_divergence<TN>(QR, rows, nf, lane);
@@ -510,7 +537,7 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(const SolveArgs a) {
         int kgp, jp;
         KM::inv(k, kgp, jp);
         const int ngp = n / TN, tp = n - ngp * TN;
-        const float* p0 = UN + (kgp + 4 * ngp) * PBS + jp * TN + tp;
+        const float* p0 = UN + pb_lane(kgp, ngp, 0) * PBS + jp * TN + tp;
         float num = 0.0f, den = 0.0f;
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) {
@@ -530,7 +557,7 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(const SolveArgs a) {
     const int rgs = lane & 7, kgs = lane >> 3;
     for (int c0 = r0; c0 < r1; c0 += kChunk) {
       const int rows = min(kChunk, r1 - c0);
-      phase_a<TK, TN>(Ws, Hs, QR, fptr, c0, rows, nf, eps, lane, vv);
+      phase_a<TK, TN>(Ws, Hs, QR, fptr, c0, rows, nf, eps, lane, vv, vt);
       if (rows == kChunk) load_v<TN>(vv, fptr, next_full(c0), nf, lane);
       __syncwarp();
       if (want_div) divacc += chunk_divergence<TN>(QR, rows, nf, lane);
@@ -646,6 +673,12 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(const SolveArgs a) {
 // change while a cluster is running (a CTA returning early would leave its
 // cluster waiting at the barrier).
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 struct FoldArgs {
   const float* stats;  // [nblk][2][KP][FP]
   const double* divpart;
@@ -672,7 +705,15 @@ struct FoldArgs {
   long long tr_cap;
   double* scale_out;  // optional: column scales s_k of this commit (batch H compensation)
   int batch_mode;
+  long long* tprof;  // ISNMF_PHASE_PROF builds: [gridDim][8] globaltimer stamps of thread 0
 };
+
+#ifdef ISNMF_PHASE_PROF
+#define FOLD_T(i) \
+  if (tid == 0 && a.tprof) a.tprof[blockIdx.x * 8 + (i)] = (long long)globaltimer_ns()
+#else
+#define FOLD_T(i)
+#endif
 
 constexpr int kFoldCluster = 4;
 constexpr int kFoldThreads = 512;
@@ -683,16 +724,12 @@ __host__ __device__ inline int fold_groups(int F) {
   const int g = kFoldThreads / nq;
   return g < 1 ? 1 : (g > 16 ? 16 : g);
 }
-// dynamic shared memory of fold_commit_kernel: row sums [2][F], W_tmp [F], group partials
+__host__ __device__ inline int fold_rows(int F) { return (F + kFoldCluster - 1) / kFoldCluster; }
+// dynamic shared memory of fold_commit_kernel: row sums [2][F], this rank's rows of
+// W, pending_a, pending_b, A, B (prefetched) and W_tmp, group partials
 __host__ __device__ inline size_t fold_smem_bytes(int F) {
   const int nq = (F + 3) / 4, g = fold_groups(F);
-  return sizeof(double) * (3 * size_t(F) + (g > 1 ? size_t(g) * nq * 8 : 0));
-}
-
-__device__ __forceinline__ unsigned long long globaltimer_ns() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
+  return sizeof(double) * (2 * size_t(F) + 6 * size_t(fold_rows(F)) + (g > 1 ? size_t(g) * nq * 8 : 0));
 }
 
 __device__ __forceinline__ unsigned cluster_rank() {
@@ -710,6 +747,11 @@ __device__ __forceinline__ const T* map_rank(const T* p, unsigned r) {
   asm volatile("mapa.u64 %0, %1, %2;" : "=l"(q) : "l"(p), "r"(r));
   return q;
 }
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // fixed-order block sum (warp tree, then warps in order); valid in thread 0
 __device__ __forceinline__ double block_sum_d(double v, double* red) {
@@ -732,21 +774,30 @@ __global__ void __cluster_dims__(kFoldCluster, 1, 1) __launch_bounds__(kFoldThre
   __shared__ double s_cs, s_sc;
   __shared__ int s_last;
   const int F = a.F, tid = threadIdx.x;
+  FOLD_T(0);
   const unsigned r = cluster_rank();
   const int k = blockIdx.x / kFoldCluster;
-  double* sums = fsm;           // [2][F]: this rank's partial sums of column k
-  double* wt = fsm + 2 * F;     // [F]: W_tmp of this rank's rows
-  double* grp = fsm + 3 * F;    // [G][NQ][8]
-  if (blockIdx.x == 0 && tid < 32) {  // divergence + counters (fixed order: lane-strided, then the warp tree)
-    double d = 0.0;
-    for (int b = tid; b < a.ndiv; b += 32) d += a.divpart[b];
-    d = warp_sum_d(d);
-    if (tid == 0) {
-      a.st->pending_div += d;
-      a.st->pending_count += (unsigned long long)a.nframes;
-      a.st->t += (unsigned long long)a.nframes;
+  const int lo = int((long long)r * F / kFoldCluster), hi = int((long long)(r + 1) * F / kFoldCluster);
+  const int R = fold_rows(F);
+  double* sums = fsm;            // [2][F]: this rank's partial sums of column k (read by the whole cluster)
+  double* rw = fsm + 2 * F;      // [R] W of rows lo..hi-1, then W_tmp
+  double* rpa = rw + R;          // [R] pending_a, then A_new
+  double* rpb = rpa + R;         // [R] pending_b, then B_new
+  double* rA = rpb + R;          // [R] A
+  double* rB = rA + R;           // [R] B
+  double* grp = rB + R;          // [G][NQ][8]
+  // the state of this rank's rows streams into shared memory behind the partial loads
+  for (int f = lo + tid; f < hi; f += kFoldThreads) {
+    const size_t cell = size_t(k) * F + f;
+    cp_async8(rw + (f - lo), a.W64 + cell);
+    cp_async8(rpa + (f - lo), a.pa + cell);
+    cp_async8(rpb + (f - lo), a.pb + cell);
+    if (a.do_commit) {
+      cp_async8(rA + (f - lo), a.A + cell);
+      cp_async8(rB + (f - lo), a.B + cell);
     }
   }
+  asm volatile("cp.async.commit_group;" ::: "memory");
   // ---- 1. this rank's share of the partial blocks, all rows of column k
   const int NQ = (F + 3) / 4, G = fold_groups(F);
   const int FP = (F + 3) & ~3;
@@ -781,6 +832,17 @@ __global__ void __cluster_dims__(kFoldCluster, 1, 1) __launch_bounds__(kFoldThre
       for (int e = 0; e < 8; ++e) grp[size_t(it) * 8 + e] = s[e];
     }
   }
+  FOLD_T(1);
+  if (blockIdx.x == 0) {  // divergence + counters (fixed order: thread-strided, then the block tree)
+    double d = 0.0;
+    for (int b = tid; b < a.ndiv; b += kFoldThreads) d += a.divpart[b];
+    d = block_sum_d(d, red);
+    if (tid == 0) {
+      a.st->pending_div += d;
+      a.st->pending_count += (unsigned long long)a.nframes;
+      a.st->t += (unsigned long long)a.nframes;
+    }
+  }
   if (G > 1) {
     __syncthreads();
     for (int f = tid; f < F; f += kFoldThreads) {
@@ -794,9 +856,10 @@ __global__ void __cluster_dims__(kFoldCluster, 1, 1) __launch_bounds__(kFoldThre
       sums[F + f] = tb;
     }
   }
-  cluster_sync_all();
+  cp_async_wait_all();
+  cluster_sync_all();  // row sums of every rank (and this thread's prefetched rows) visible
+  FOLD_T(2);
   // ---- 2. rows [lo, hi) of column k: cluster-wide sums in rank order, pending / commit part 1
-  const int lo = int((long long)r * F / kFoldCluster), hi = int((long long)(r + 1) * F / kFoldCluster);
   double cs = 0.0;
   unsigned bad = 0;
   for (int f = lo + tid; f < hi; f += kFoldThreads) {
@@ -807,19 +870,18 @@ __global__ void __cluster_dims__(kFoldCluster, 1, 1) __launch_bounds__(kFoldThre
       ta += rs[f];
       tb += rs[F + f];
     }
+    const int j = f - lo;
     const size_t cell = size_t(k) * F + f;
-    const double w = a.W64[cell];
-    const double pa = a.pa[cell] + w * w * ta;
-    const double pb = a.pb[cell] + tb;
+    const double w = rw[j];
+    const double pa = rpa[j] + w * w * ta;
+    const double pb = rpb[j] + tb;
     if (!a.do_commit) {
       a.pa[cell] = pa;
       a.pb[cell] = pb;
       continue;
     }
-    const double An = a.rho * a.A[cell] + pa;  // rho scales the past (online.hpp:319-320)
-    const double Bn = a.rho * a.B[cell] + pb;
-    a.A[cell] = An;
-    a.B[cell] = Bn;
+    const double An = a.rho * rA[j] + pa;  // rho scales the past (online.hpp:319-320)
+    const double Bn = a.rho * rB[j] + pb;
     a.pa[cell] = 0.0;
     a.pb[cell] = 0.0;
     double wn = w;
@@ -828,7 +890,9 @@ __global__ void __cluster_dims__(kFoldCluster, 1, 1) __launch_bounds__(kFoldThre
     else if (An > 0.0)
       bad |= ST_INCONSISTENT;
     if (!isfinite(wn)) bad |= ST_NONFINITE_W;
-    wt[f] = wn;
+    rpa[j] = An;
+    rpb[j] = Bn;
+    rA[j] = wn;  // W_tmp (rw keeps the old W for ||dW||)
     cs += wn;
   }
   if (!a.do_commit) {
@@ -836,9 +900,11 @@ __global__ void __cluster_dims__(kFoldCluster, 1, 1) __launch_bounds__(kFoldThre
     return;
   }
   if (bad) atomicOr(&a.st->pad, bad);
+  FOLD_T(3);
   cs = block_sum_d(cs, red);
   if (tid == 0) s_cs = cs;
   cluster_sync_all();
+  FOLD_T(4);
   // ---- 3. column scale s_k (rank order), rescale of this rank's rows
   if (tid == 0) {
     double sc = 0.0;
@@ -847,27 +913,32 @@ __global__ void __cluster_dims__(kFoldCluster, 1, 1) __launch_bounds__(kFoldThre
   }
   cluster_sync_all();  // s_sc visible; no rank reads another's shared memory after this
   const double sc = s_sc;
+  const bool ok = sc > 0.0;
   double d2 = 0.0, cw = 0.0;
-  if (!(sc > 0.0)) {
-    if (tid == 0) atomicOr(&a.st->pad, ST_ZERO_COLUMN);
-  } else {
-    for (int f = lo + tid; f < hi; f += kFoldThreads) {
-      const size_t cell = size_t(k) * F + f;
-      const double wn = wt[f] / sc;
-      const double d = wn - a.W64[cell];
-      d2 += d * d;
-      cw += wn;
-      a.W64[cell] = wn;
-      a.A[cell] /= sc;
-      a.B[cell] *= sc;
-      a.W32[size_t(f) * a.WS + k] = float(wn);
+  for (int f = lo + tid; f < hi; f += kFoldThreads) {
+    const int j = f - lo;
+    const size_t cell = size_t(k) * F + f;
+    if (!ok) {  // ZeroColumn: A, B committed, W unchanged (the status aborts the run)
+      a.A[cell] = rpa[j];
+      a.B[cell] = rpb[j];
+      continue;
     }
-    if (r == 0 && tid == 0) {
-      const unsigned long long c = a.st->commits;
-      a.P[size_t(c + 1) * a.K + k] = a.P[size_t(c) * a.K + k] * sc;
-      if (a.scale_out) a.scale_out[k] = sc;
-    }
+    const double wn = rA[j] / sc;
+    const double d = wn - rw[j];
+    d2 += d * d;
+    cw += wn;
+    a.W64[cell] = wn;
+    a.A[cell] = rpa[j] / sc;
+    a.B[cell] = rpb[j] * sc;
+    a.W32[size_t(f) * a.WS + k] = float(wn);
   }
+  if (ok && r == 0 && tid == 0) {
+    const unsigned long long c = a.st->commits;
+    a.P[size_t(c + 1) * a.K + k] = a.P[size_t(c) * a.K + k] * sc;
+    if (a.scale_out) a.scale_out[k] = sc;
+  }
+  if (!ok && tid == 0) atomicOr(&a.st->pad, ST_ZERO_COLUMN);
+  FOLD_T(5);
   d2 = block_sum_d(d2, red);
   cw = block_sum_d(cw, red);
   if (tid == 0) {
@@ -877,6 +948,7 @@ __global__ void __cluster_dims__(kFoldCluster, 1, 1) __launch_bounds__(kFoldThre
     s_last = atomicAdd(&a.st->ticket, 1u) == gridDim.x - 1;
   }
   __syncthreads();
+  FOLD_T(6);
   if (!s_last) return;
   // ---- 4. last CTA: ||dW||_F, mean W, objective, trace point, stop rule
   __threadfence();
@@ -888,29 +960,32 @@ __global__ void __cluster_dims__(kFoldCluster, 1, 1) __launch_bounds__(kFoldThre
   pd = block_sum_d(pd, red);
   pw = block_sum_d(pw, red);
   if (tid == 0) {
-    DevState* st = a.st;
+    volatile DevState* st = a.st;
+    const unsigned int err = st->pad;
+    const unsigned long long c = st->commits, t = st->t, pc = st->pending_count, tb = st->trace_base;
+    const double pdiv = st->pending_div;
     st->ticket = 0;
-    const unsigned int err = *reinterpret_cast<volatile unsigned int*>(&st->pad);
     st->pad = 0;
     if (err) {
       st->status |= err;
       return;
     }
-    const unsigned long long c = st->commits;
-    st->last_delta = sqrt(pd);
+    const double delta = sqrt(pd), obj = pc ? pdiv / double(pc) : 0.0;
+    st->last_delta = delta;
     st->kmeanw = double(a.K) * (pw / (double(a.F) * double(a.K)));
-    st->last_obj = st->pending_count ? st->pending_div / double(st->pending_count) : 0.0;
-    const long long ti = (long long)(c - st->trace_base);
+    st->last_obj = obj;
+    const long long ti = (long long)(c - tb);
     if (a.tr_t && ti >= 0 && ti < a.tr_cap) {
-      a.tr_t[ti] = st->t;
-      a.tr_obj[ti] = st->last_obj;
+      a.tr_t[ti] = t;
+      a.tr_obj[ti] = obj;
       a.tr_ns[ti] = globaltimer_ns();
     }
     st->pending_div = 0.0;
     st->pending_count = 0;
     st->commits = c + 1;
-    if (!a.batch_mode && a.eta > 0.0 && st->last_delta < a.eta) *a.halt = 1u;
+    if (!a.batch_mode && a.eta > 0.0 && delta < a.eta) *a.halt = 1u;
   }
+  FOLD_T(7);
 }
 
 // ---------------------------------------------------------------------------

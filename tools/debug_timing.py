@@ -29,3 +29,11 @@ for rep in range(4):
     print(f"rep {rep}: enqueue {1e3*(t1-t0):.2f} ms, sync {1e3*(t2-t1):.2f} ms, span {k['span_ms']:.2f} ms, "
           f"k1 {k['solve_ms']:.2f} ms / {k['solve_launches']} launches, k2+k3 {k['tail_ms']:.2f} ms, "
           f"frames/s {N/(k['span_ms']/1e3):.3e}")
+# without per-kernel events: wall time of enqueue+synchronize
+for rep in range(3):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    eng.enqueue(vd, N, vd.stride(0))
+    eng.synchronize()
+    t2 = time.perf_counter()
+    print(f"no-events rep {rep}: wall {1e3*(t2-t0):.2f} ms, frames/s {N/(t2-t0):.3e}")
