@@ -171,12 +171,13 @@ int isnmf_online_get_last_h(isnmf_online* ctx, double* h, int64_t n);
 /* Number of engine kernel launches issued so far (bench accounting). */
 int64_t isnmf_online_launch_count(isnmf_online* ctx);
 
-/* Profiling: between begin and end, CUDA events are recorded on the engine's
- * compute stream around every K1 (solve) launch and around each K2+K3
- * (reduce + commit) pair.  end() waits for the stream and returns the summed K1
- * device time, the K1 launch and frame counts, the device time of the whole
- * region on that stream and the summed K2+K3 time. */
-int isnmf_online_profile_begin(isnmf_online* ctx);
+/* Profiling: begin() records a CUDA event on the engine's compute stream; with
+ * per_kernel != 0 events are also recorded around every K1 (solve) and K2
+ * (fold/commit) launch (they add ~2 us per mini-batch).  end() records the
+ * closing event, waits for the stream and returns the summed K1 device time,
+ * the K1 launch and frame counts, the device time of the whole region on that
+ * stream and the summed K2 time (the per-kernel values are 0 without per_kernel). */
+int isnmf_online_profile_begin(isnmf_online* ctx, int32_t per_kernel);
 int isnmf_online_profile_end(isnmf_online* ctx, double* solve_ms, int64_t* solve_launches, int64_t* solve_frames,
                              double* span_ms, double* tail_ms);
 

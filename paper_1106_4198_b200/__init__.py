@@ -72,7 +72,7 @@ _SIGS = {
     "isnmf_online_commit": ([VP], C.c_int),
     "isnmf_host_alloc": ([I64], VP),
     "isnmf_host_free": ([VP], None),
-    "isnmf_online_profile_begin": ([VP], C.c_int),
+    "isnmf_online_profile_begin": ([VP, C.c_int32], C.c_int),
     "isnmf_online_profile_end": ([VP, VP, VP, VP, VP, VP], C.c_int),
     "isnmf_batch_train": ([VP, I64, I64, I64, I64, VP, VP, U64, D, D, VP, VP, VP, VP, VP, VP], C.c_int),
 }
@@ -275,14 +275,16 @@ class Online:
 
 
 class Profile:
-    """CUDA events around every K1 launch on the engine's own stream."""
+    """CUDA events on the engine's own stream: the whole region, and with
+    per_kernel=True also around every K1 / K2 launch."""
 
-    def __init__(self, online):
+    def __init__(self, online, per_kernel=True):
         self.o = online
+        self.per_kernel = per_kernel
         self._span = None
 
     def start(self):
-        _check(lib().isnmf_online_profile_begin(self.o._h))
+        _check(lib().isnmf_online_profile_begin(self.o._h, 1 if self.per_kernel else 0))
 
     def stop(self):
         ms, nl, nf, span, tail = D(), I64(), I64(), D(), D()

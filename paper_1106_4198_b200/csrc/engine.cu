@@ -313,6 +313,7 @@ struct isnmf_online {
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
+  bool span_open = false;           // between profile_begin and profile_end
   std::vector<cudaEvent_t> ev_tail;  // K2 start, K3 end per mini-batch (profiling)
   size_t tail_used = 0;
   int64_t prof_frames = 0;
@@ -962,11 +963,12 @@ int isnmf_debug_fold_prof(isnmf_online* c, long long* out, int64_t cap) {
 }
 #endif
 
-int isnmf_online_profile_begin(isnmf_online* c) {
+int isnmf_online_profile_begin(isnmf_online* c, int32_t per_kernel) {
   if (!c) return fail(ISNMF_E_INVALID_ARG, "NULL context");
   for (int i = 0; i < 2; ++i)
     if (!c->ev_span[i]) CU(cudaEventCreate(&c->ev_span[i]));
-  c->prof = true;
+  c->prof = per_kernel != 0;
+  c->span_open = true;
   c->ev_used = 0;
   c->tail_used = 0;
   c->prof_frames = 0;
@@ -976,7 +978,7 @@ int isnmf_online_profile_begin(isnmf_online* c) {
 
 int isnmf_online_profile_end(isnmf_online* c, double* solve_ms, int64_t* solve_launches, int64_t* solve_frames,
                              double* span_ms, double* tail_ms) {
-  if (!c || !c->prof) return fail(ISNMF_E_INVALID_ARG, "profile_end without profile_begin");
+  if (!c || !c->span_open) return fail(ISNMF_E_INVALID_ARG, "profile_end without profile_begin");
   CU(cudaEventRecord(c->ev_span[1], c->cs));
   CU(cudaEventSynchronize(c->ev_span[1]));
   double tot = 0.0;
@@ -999,6 +1001,7 @@ int isnmf_online_profile_end(isnmf_online* c, double* solve_ms, int64_t* solve_l
   if (solve_frames) *solve_frames = c->prof_frames;
   if (span_ms) *span_ms = span;
   c->prof = false;
+  c->span_open = false;
   return 0;
 }
 
