@@ -14,19 +14,23 @@
 #pragma once
 
 #include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <deque>
+#include <fstream>
 #include <functional>
 #include <istream>
 #include <limits>
 #include <memory>
 #include <numeric>
 #include <optional>
+#include <string>
 #include <utility>
 #include <vector>
 
 #include "batch.hpp"
+#include "io.hpp"
 #include "kernels.hpp"
 #include "model.hpp"
 #include "report.hpp"
@@ -164,7 +168,9 @@ class GeneratorSource final : public SampleSource {
 };
 
 /// Headerless chunked wire format [u64 LE count | count x F f64 LE], permuted
-/// per buffer; not seekable (online.hpp:154-220).
+/// per buffer; not seekable (online.hpp:151-220).  Frames are decoded into one
+/// contiguous fp64 block per buffer (no per-frame allocation); next_block
+/// converts them straight into the engine's pinned fp32 staging.
 class ChunkStreamSource final : public SampleSource {
  public:
   ChunkStreamSource(std::istream& in, Index rows, std::size_t buffer_frames, std::uint64_t seed)
@@ -172,48 +178,74 @@ class ChunkStreamSource final : public SampleSource {
     if (rows < 1) throw ShapeMismatch("ChunkStreamSource: rows must be >= 1");
   }
   std::optional<Sample> next() override {
-    if (ready_.empty() && !refill()) return std::nullopt;
-    Sample s{std::move(ready_.front()), t_++};
-    ready_.pop_front();
-    return s;
+    if (pos_ == order_.size() && !refill()) return std::nullopt;
+    const double* src = block_.data() + order_[pos_++] * std::size_t(rows_);
+    Vector v(rows_);
+    std::memcpy(v.data(), src, std::size_t(rows_) * sizeof(double));
+    return Sample{std::move(v), t_++};
+  }
+  std::size_t next_block(std::size_t n, Index F, float* dst, std::uint64_t* index) override {
+    if (F != rows_) throw ShapeMismatch("online_step: frame size vs dictionary rows");
+    std::size_t m = 0;
+    while (m < n) {
+      if (pos_ == order_.size() && !refill()) break;
+      const std::size_t take = std::min(n - m, order_.size() - pos_);
+      for (std::size_t i = 0; i < take; ++i) {
+        const double* src = block_.data() + order_[pos_ + i] * std::size_t(F);
+        float* out = dst + (m + i) * std::size_t(F);
+        for (Index f = 0; f < F; ++f) out[f] = float(src[f]);
+        index[m + i] = t_++;
+      }
+      pos_ += take;
+      m += take;
+    }
+    return m;
   }
   void seek(std::uint64_t) override { throw IoError("ChunkStreamSource: stream input is not seekable"); }
   std::optional<std::uint64_t> size() const override { return std::nullopt; }
 
  private:
-  static std::uint64_t le64(const unsigned char* p) {
-    std::uint64_t v = 0;
-    for (int i = 7; i >= 0; --i) v = (v << 8) | p[i];
-    return v;
-  }
+  std::size_t pending_frames() const { return pending_.size() / std::size_t(rows_); }
+  // one chunk appended to pending_ (false at a clean end of stream)
   bool read_chunk() {
     unsigned char head[8];
     in_->read(reinterpret_cast<char*>(head), 8);
     if (in_->gcount() == 0) return false;
     if (in_->gcount() != 8) throw TruncatedPayload("stream chunk header truncated");
-    const std::uint64_t count = le64(head);
-    std::vector<unsigned char> raw(static_cast<size_t>(rows_) * 8);
-    for (std::uint64_t c = 0; c < count; ++c) {
+    std::uint64_t count = 0;
+    for (int i = 7; i >= 0; --i) count = (count << 8) | head[i];
+    const std::size_t F = std::size_t(rows_);
+    constexpr std::uint64_t kPiece = 4096;  // frames decoded per read
+    std::vector<unsigned char> raw;
+    for (std::uint64_t done = 0; done < count;) {
+      const std::size_t nf = std::size_t(std::min(kPiece, count - done));
+      raw.resize(nf * F * 8);
       in_->read(reinterpret_cast<char*>(raw.data()), std::streamsize(raw.size()));
       if (in_->gcount() != std::streamsize(raw.size())) throw TruncatedPayload("stream frame truncated");
-      Vector frame(rows_);
-      for (Index f = 0; f < rows_; ++f) {
-        const std::uint64_t bits = le64(raw.data() + 8 * f);
-        std::memcpy(&frame[f], &bits, 8);
-        if (!std::isfinite(frame[f]) || frame[f] < 0.0) throw NonFiniteEntry("stream frame with invalid entries");
+      const std::size_t base = pending_.size();
+      pending_.resize(base + nf * F);
+      for (std::size_t i = 0; i < nf * F; ++i) {
+        std::uint64_t bits = 0;
+        for (int b = 7; b >= 0; --b) bits = (bits << 8) | raw[8 * i + std::size_t(b)];
+        double x;
+        std::memcpy(&x, &bits, 8);
+        if (!std::isfinite(x) || x < 0.0) throw NonFiniteEntry("stream frame with invalid entries");
+        pending_[base + i] = x;
       }
-      pending_.push_back(std::move(frame));
+      done += nf;
     }
     return true;
   }
   bool refill() {
-    while (pending_.size() < buffer_ && read_chunk()) {
+    while (pending_frames() < buffer_ && read_chunk()) {
     }
     if (pending_.empty()) return false;
-    const std::size_t len = std::min(buffer_, pending_.size());
-    for (std::uint64_t i : detail::shuffled_range(len, seed_, block_++))
-      ready_.push_back(std::move(pending_[static_cast<std::size_t>(i)]));
-    pending_.erase(pending_.begin(), pending_.begin() + static_cast<std::ptrdiff_t>(len));
+    const std::size_t len = std::min(buffer_, pending_frames());
+    const std::size_t F = std::size_t(rows_);
+    block_.assign(pending_.begin(), pending_.begin() + std::ptrdiff_t(len * F));
+    pending_.erase(pending_.begin(), pending_.begin() + std::ptrdiff_t(len * F));
+    order_ = detail::shuffled_range(len, seed_, blocks_++);
+    pos_ = 0;
     return true;
   }
   std::istream* in_;
@@ -221,9 +253,11 @@ class ChunkStreamSource final : public SampleSource {
   std::size_t buffer_;
   std::uint64_t seed_;
   std::uint64_t t_ = 0;
-  std::uint64_t block_ = 0;
-  std::vector<Vector> pending_;
-  std::deque<Vector> ready_;
+  std::uint64_t blocks_ = 0;
+  std::vector<double> pending_;  // frames read ahead, arrival order
+  std::vector<double> block_;    // the current buffer
+  std::vector<std::uint64_t> order_;
+  std::size_t pos_ = 0;
 };
 
 namespace detail {
@@ -492,6 +526,75 @@ inline OnlineState online_train(SampleSource& source, const SolverConfig& config
   OnlineState state = make_online_state(w0, config, source.size(), source.dataset());
   online_resume(state, source, config, callback, clock);
   return state;
+}
+
+// --- checkpoints (online.hpp:421-489) ------------------------------------
+// "ISCK" | u32 version | u32 restart (0 warm, 1 fresh) | u64 t | u64 seed |
+// u64 commits | f64 rho (as u64 bits) | matrices W, A, B, pending_a,
+// pending_b [, warm_h in warm mode].  The host fields are the state of record
+// (online_resume pulls them from the device before returning), and the
+// per-sample randomness is a function of (seed, t), so a fresh-mode run
+// resumed from a checkpoint reproduces the uninterrupted one bit-exactly.
+
+inline constexpr char kCheckpointMagic[4] = {'I', 'S', 'C', 'K'};
+inline constexpr std::uint32_t kCheckpointFormatVersion = 1;
+
+inline void save_checkpoint(std::ostream& out, const OnlineState& st) {
+  detail::put_raw(out, kCheckpointMagic, 4);
+  detail::put_le<std::uint32_t>(out, kCheckpointFormatVersion);
+  detail::put_le<std::uint32_t>(out, st.restart == RestartMode::warm ? 0u : 1u);
+  detail::put_le<std::uint64_t>(out, st.t);
+  detail::put_le<std::uint64_t>(out, st.seed);
+  detail::put_le<std::uint64_t>(out, st.commits);
+  std::uint64_t rho_bits;
+  std::memcpy(&rho_bits, &st.rho, 8);
+  detail::put_le<std::uint64_t>(out, rho_bits);
+  save_matrix(out, st.dict.w);
+  save_matrix(out, st.dict.a);
+  save_matrix(out, st.dict.b);
+  save_matrix(out, st.pending_a);
+  save_matrix(out, st.pending_b);
+  if (st.restart == RestartMode::warm) save_matrix(out, st.warm_h);
+}
+
+inline void save_checkpoint(const std::string& path, const OnlineState& st) {
+  std::ofstream out(path, std::ios::binary);
+  if (!out) throw IoError("cannot open for writing: " + path);
+  save_checkpoint(out, st);
+  out.flush();
+  if (!out) throw IoError("write failed: " + path);
+}
+
+inline OnlineState load_checkpoint(std::istream& in) {
+  char magic[4];
+  detail::get_raw(in, magic, 4, "checkpoint magic");
+  if (std::memcmp(magic, kCheckpointMagic, 4) != 0) throw BadMagic("not a checkpoint file");
+  const auto version = detail::get_le<std::uint32_t>(in, "checkpoint version");
+  if (version != kCheckpointFormatVersion) throw BadMagic("unsupported checkpoint version " + std::to_string(version));
+  const auto restart = detail::get_le<std::uint32_t>(in, "restart mode");
+  if (restart > 1) throw UnsupportedFormat("invalid restart mode in checkpoint");
+  OnlineState st;
+  st.restart = restart == 0 ? RestartMode::warm : RestartMode::fresh;
+  st.t = detail::get_le<std::uint64_t>(in, "t");
+  st.seed = detail::get_le<std::uint64_t>(in, "seed");
+  st.commits = detail::get_le<std::uint64_t>(in, "commits");
+  const auto rho_bits = detail::get_le<std::uint64_t>(in, "rho");
+  std::memcpy(&st.rho, &rho_bits, 8);
+  st.dict.w = load_matrix(in);
+  st.dict.a = load_matrix(in);
+  st.dict.b = load_matrix(in);
+  st.pending_a = load_matrix(in);
+  st.pending_b = load_matrix(in);
+  if (st.restart == RestartMode::warm) st.warm_h = load_matrix(in);
+  st.trace.stage = "online";
+  st.trace.seed = st.seed;
+  return st;
+}
+
+inline OnlineState load_checkpoint(const std::string& path) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw IoError("cannot open: " + path);
+  return load_checkpoint(in);
 }
 
 }  // namespace isnmf

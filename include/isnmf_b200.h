@@ -191,6 +191,16 @@ int isnmf_batch_train(const float* v, int64_t ldv, int64_t F, int64_t N, int64_t
                       const double* h0, uint64_t max_epochs, double epsilon, double eta, double* w_out,
                       double* h_out, double* obj_trace, uint64_t* epochs, double* initial_obj, double* last_delta);
 
+/* ---------------------------------------------------------------------------
+ * Held-out fit — evaluate_heldout (harness.hpp:17-37): H from the reference's
+ * seed-deterministic uniform stream scaled by max(mean test, eps)/(K mean W),
+ * inner_iters MM updates at frozen W (the fused solve kernel, no statistics),
+ * then the mean IS divergence per frame.  test: F x N fp32 with leading
+ * dimension ldt (host or device); w: F x K fp64.  W is not modified.
+ * ------------------------------------------------------------------------- */
+int isnmf_evaluate_heldout(const float* test, int64_t ldt, int64_t F, int64_t N, const double* w, int64_t K,
+                           double epsilon, int32_t inner_iters, uint64_t seed, double* out);
+
 #ifdef __cplusplus
 }
 #endif

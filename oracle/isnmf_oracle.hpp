@@ -365,6 +365,27 @@ inline Mat default_h0(const Mat& v, const Mat& w, double eps) {
   return Mat(w.c, v.c, scale);
 }
 
+// harness.hpp:17-37 — held-out fit: H from one seed-deterministic stream of
+// open-interval uniforms (column-major fill) scaled by max(mean V, eps)/(K mean W),
+// `iters` MM updates at frozen W, then the mean divergence per frame.
+inline Mat heldout_h0(const Mat& w, const Mat& test, double eps, uint64_t seed) {
+  const double scale = std::max(mean(test.d.data(), test.size()), eps) / (double(w.c) * mean(w.d.data(), w.size()));
+  std::mt19937_64 g = make_engine(mix_seed(seed, 0xE7A1ULL));
+  Mat h(w.c, test.c);
+  for (int64_t j = 0; j < h.c; ++j)
+    for (int64_t i = 0; i < h.r; ++i) h(i, j) = scale * uniform_open01(g);
+  return h;
+}
+
+inline double evaluate_heldout(const Mat& w, const Mat& test, double eps, int iters, uint64_t seed) {
+  if (w.r != test.r) throw Error(SHAPE_MISMATCH, "evaluate_heldout: W rows vs test rows");
+  if (test.c == 0) throw Error(EMPTY_DATASET, "evaluate_heldout: empty test set");
+  Mat h = heldout_h0(w, test, eps, seed);
+  std::vector<double> approx, ratio;
+  for (int64_t j = 0; j < test.c; ++j) solve_h(test.col(j), w, h.col(j), iters, eps, approx, ratio);
+  return objective(test, w, h, eps);
+}
+
 // ---- sample orders (reference online.hpp:53-149) ------------------------------
 // CyclingSource::load_cycle (online.hpp:79-87): Fisher-Yates of [0,n).
 inline std::vector<uint64_t> cycle_permutation(uint64_t seed, uint64_t cycle, uint64_t n) {

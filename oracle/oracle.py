@@ -218,6 +218,24 @@ def default_h0(v, w, eps=1e-12):
     return h
 
 
+def evaluate_heldout(w, test, eps=1e-12, inner_iters=100, seed=0x45):
+    """harness.hpp:17-37."""
+    w, test = _fortran(w), _fortran(test)
+    out = D()
+    _check(lib().oracle_evaluate_heldout(_p(w), _p(test), I64(w.shape[0]), I64(w.shape[1]), I64(test.shape[0]),
+                                         I64(test.shape[1]), D(eps), C.c_int(inner_iters), C.c_uint64(seed),
+                                         C.byref(out)))
+    return out.value
+
+
+def heldout_h0(w, test, eps=1e-12, seed=0x45):
+    w, test = _fortran(w), _fortran(test)
+    h = np.empty((w.shape[1], test.shape[1]), order="F")
+    _check(lib().oracle_heldout_h0(_p(w), _p(test), I64(w.shape[0]), I64(w.shape[1]), I64(test.shape[1]), D(eps),
+                                   C.c_uint64(seed), _p(h)))
+    return h
+
+
 def init_from_samples(v, k, seed, eps=1e-12):
     v = _fortran(v)
     w = np.empty((v.shape[0], k), order="F")

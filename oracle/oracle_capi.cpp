@@ -153,6 +153,15 @@ int oracle_default_h0(const double* v, const double* w, int64_t F, int64_t K, in
   return guard([&] { unwrap(default_h0(wrap(v, F, N), wrap(w, F, K), eps), h); });
 }
 
+int oracle_evaluate_heldout(const double* w, const double* test, int64_t F, int64_t K, int64_t Ft, int64_t N,
+                            double eps, int iters, uint64_t seed, double* out) {
+  return guard([&] { *out = evaluate_heldout(wrap(w, F, K), wrap(test, Ft, N), eps, iters, seed); });
+}
+int oracle_heldout_h0(const double* w, const double* test, int64_t F, int64_t K, int64_t N, double eps, uint64_t seed,
+                      double* h) {
+  return guard([&] { unwrap(heldout_h0(wrap(w, F, K), wrap(test, F, N), eps, seed), h); });
+}
+
 // ---- online trainer ----
 struct OracleOnline {
   Online st;

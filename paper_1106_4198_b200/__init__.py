@@ -75,6 +75,7 @@ _SIGS = {
     "isnmf_online_profile_begin": ([VP, C.c_int32], C.c_int),
     "isnmf_online_profile_end": ([VP, VP, VP, VP, VP, VP], C.c_int),
     "isnmf_batch_train": ([VP, I64, I64, I64, I64, VP, VP, U64, D, D, VP, VP, VP, VP, VP, VP], C.c_int),
+    "isnmf_evaluate_heldout": ([VP, I64, I64, I64, VP, I64, D, C.c_int32, U64, VP], C.c_int),
 }
 
 
@@ -315,3 +316,17 @@ def batch_train(v32, w0, h0, max_epochs, eps=1e-12, eta=0.0):
     _check(lib().isnmf_batch_train(_p(v32), ldv, F, N, K, _p(w0), _p(h0), max_epochs, eps, eta, _p(w), _p(h),
                                    _p(obj), C.byref(ep), C.byref(o0), C.byref(ld)))
     return dict(w=w, h=h, obj=obj[:ep.value].copy(), epochs=ep.value, initial_obj=o0.value, last_delta=ld.value)
+
+
+def evaluate_heldout(test32, w, eps=1e-12, inner_iters=100, seed=0x45):
+    """harness.hpp:17-37 on the device. test32: F x N fp32 numpy (or torch [N, ldt])."""
+    w = _f(w)
+    F, K = w.shape
+    if hasattr(test32, "data_ptr"):
+        ldt, N = test32.stride(0), test32.shape[0]
+    else:
+        test32 = np.asfortranarray(test32, dtype=np.float32)
+        ldt, N = F, test32.shape[1]
+    out = D()
+    _check(lib().isnmf_evaluate_heldout(_p(test32), ldt, F, N, _p(w), K, eps, inner_iters, seed, C.byref(out)))
+    return out.value

@@ -16,6 +16,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <random>
 #include <string>
 #include <unordered_set>
 #include <vector>
@@ -1064,6 +1065,35 @@ __global__ void rescale_kernel(double* w, double* a, double* b, int64_t F, int64
     for (int64_t n = threadIdx.x; n < N; n += blockDim.x) h[n * K + k] *= sc;
 }
 
+// Deterministic fp64 sum of an F x N fp32 matrix with leading dimension ld:
+// block b sums a fixed element range (thread-strided, block tree), then one
+// block adds the partials in block order.
+constexpr int kSumBlocks = 296, kSumThreads = 256;
+__global__ void sum_f32_partial(const float* v, int64_t ld, int64_t F, int64_t N, double* part) {
+  __shared__ double sh[kSumThreads];
+  const int64_t n = F * N, per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t e0 = blockIdx.x * per, e1 = std::min<int64_t>(n, e0 + per);
+  double s = 0.0;
+  for (int64_t e = e0 + threadIdx.x; e < e1; e += kSumThreads) {
+    const int64_t j = e / F, f = e - j * F;
+    s += double(v[j * ld + f]);
+  }
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = kSumThreads / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+__global__ void sum_partials(const double* part, int n, double* out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s += part[i];
+    *out = s;
+  }
+}
+
 // A device workspace for the fused solve over an arbitrary set of frames.
 struct SolveWork {
   int F = 0, K = 0, WS = 0, KP = 0, NT = 0;
@@ -1474,6 +1504,76 @@ int isnmf_batch_train(const float* v, int64_t ldv, int64_t F, int64_t N, int64_t
   for (size_t i = 0; i < h32.size(); ++i) h_out[i] = h32[i];
   if (epochs) *epochs = done;
   if (last_delta) *last_delta = delta;
+  return 0;
+}
+
+// harness.hpp:17-37.  H0 = max(mean test, eps)/(K mean W) * uniform_open01 from
+// the reference stream mt19937_64(splitmix64(mix_seed(seed, 0xE7A1))), filled
+// column-major; the stream is sequential, so it is drawn on the host (std::
+// mt19937_64 is specified bit-exactly by the standard) and uploaded; the scale
+// is applied on the device (hscale).  The MM iterations and the divergence of
+// the final fit run in the fused solve kernel at frozen W.
+int isnmf_evaluate_heldout(const float* test, int64_t ldt, int64_t F, int64_t N, const double* w, int64_t K,
+                           double eps, int32_t inner_iters, uint64_t seed, double* out) {
+  if (!test || !w || !out) return fail(ISNMF_E_INVALID_ARG, "NULL argument");
+  if (F < 1 || K < 1 || ldt < F) return fail(ISNMF_E_SHAPE_MISMATCH, "evaluate_heldout: W rows vs test rows");
+  if (N == 0) return fail(ISNMF_E_EMPTY_DATASET, "evaluate_heldout: empty test set");
+  if (!(eps > 0.0)) return fail(ISNMF_E_NEGATIVE_INPUT, "epsilon must be > 0");
+  if (inner_iters < 0) return fail(ISNMF_E_INVALID_ARG, "evaluate_heldout: inner_iters < 0");
+  double wsum = 0.0;
+  for (int64_t i = 0; i < F * K; ++i) wsum += w[i];
+  const double wmean = wsum / double(F * K);
+  SolveWork wk;
+  TRY(wk.init(F, K, N));
+  TRY(wk.set_w(w));
+  DevBuf bv, bh, bs, bp;
+  const float* dv = test;
+  int64_t dld = ldt;
+  if (!is_device_ptr(test)) {
+    float* tmp = nullptr;
+    TRY(dalloc(&tmp, size_t(F) * N));
+    CU(cudaMemcpy2D(tmp, size_t(F) * sizeof(float), test, size_t(ldt) * sizeof(float), size_t(F) * sizeof(float),
+                    size_t(N), cudaMemcpyHostToDevice));
+    bv.p = tmp;
+    dv = tmp;
+    dld = F;
+  }
+  // scale = max(mean(test), eps) / (K * mean(W)), the mean reduced on the device
+  double* part = nullptr;
+  TRY(dalloc(&part, kSumBlocks + 1));
+  bp.p = part;
+  sum_f32_partial<<<kSumBlocks, kSumThreads, 0, wk.s>>>(dv, dld, F, N, part);
+  sum_partials<<<1, 32, 0, wk.s>>>(part, kSumBlocks, part + kSumBlocks);
+  double tsum = 0.0;
+  CU(cudaMemcpyAsync(&tsum, part + kSumBlocks, sizeof(double), cudaMemcpyDeviceToHost, wk.s));
+  // uniforms (host stream, overlapped with the reduction)
+  std::vector<float> u(size_t(K) * N);
+  {
+    auto sm = [](uint64_t x) {
+      x += 0x9e3779b97f4a7c15ULL;
+      x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+      x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+      return x ^ (x >> 31);
+    };
+    const uint64_t stream = sm(sm(seed) ^ sm(~uint64_t(0xE7A1)));
+    std::mt19937_64 g(sm(stream));
+    for (size_t i = 0; i < u.size(); ++i) u[i] = float(1.0 - double(g() >> 11) * 0x1.0p-53);
+  }
+  CU(cudaStreamSynchronize(wk.s));
+  const double scale = std::max(tsum / double(F * N), eps) / (double(K) * wmean);
+  float* dh = nullptr;
+  TRY(dalloc(&dh, u.size()));
+  bh.p = dh;
+  CU(cudaMemcpyAsync(dh, u.data(), u.size() * sizeof(float), cudaMemcpyHostToDevice, wk.s));
+  double* dscale = nullptr;
+  TRY(dalloc(&dscale, size_t(K)));
+  bs.p = dscale;
+  fill_f64<<<1, 256, 0, wk.s>>>(dscale, K, scale);
+  TRY(wk.pass(dv, dld, N, dh, inner_iters, eps, dscale, false, false, true));
+  DevState h{};
+  TRY(wk.state(&h));
+  if (h.status) return status_to_code(h.status, "evaluate_heldout", 0);
+  *out = h.pending_div / double(N);
   return 0;
 }
 

@@ -302,3 +302,64 @@ TEST_CASE("batch_train descends and equals online at beta = N, r = 0 (SPEC.md:40
 }
 
 MT_MAIN()
+
+TEST_CASE("checkpoint/resume at a commit boundary reproduces the uninterrupted run bitwise (SPEC.md:418)") {
+  const Index F = 65, K = 4, N = 96;
+  Matrix v = spectrogram(F, K, N, 31);
+  Matrix w0 = normalized(random_positive(F, K, 32, 0.1, 1.0));
+  SolverConfig c;
+  c.k = int(K);
+  c.beta = 16;
+  c.restart = RestartMode::fresh;
+  c.inner_iters = 6;
+  c.eta = 0.0;
+  c.seed = 9;
+  c.max_epochs_or_samples = 2 * N;
+  CyclingSource full_src(v, 5);
+  OnlineState full = online_train(full_src, c, w0);
+  // same run, stopped at t = 80 (a commit boundary), saved, reloaded, resumed
+  c.max_epochs_or_samples = 80;
+  CyclingSource src(v, 5);
+  OnlineState half = online_train(src, c, w0);
+  std::stringstream ss;
+  save_checkpoint(ss, half);
+  OnlineState back = load_checkpoint(ss);
+  back.trace.config = c;
+  c.max_epochs_or_samples = 2 * N;
+  online_resume(back, src, c);
+  CHECK(back.t == full.t && back.commits == full.commits);
+  CHECK(std::memcmp(back.dict.w.data(), full.dict.w.data(), size_t(F * K) * sizeof(double)) == 0);
+  CHECK(std::memcmp(back.dict.a.data(), full.dict.a.data(), size_t(F * K) * sizeof(double)) == 0);
+  CHECK(std::memcmp(back.dict.b.data(), full.dict.b.data(), size_t(F * K) * sizeof(double)) == 0);
+  // mid-mini-batch checkpoint: pending statistics travel in the file; the split
+  // launch sums the same frames in another grouping (fp32 partials), so W agrees
+  // to the fp32 level rather than bitwise
+  c.max_epochs_or_samples = 87;
+  CyclingSource src2(v, 5);
+  OnlineState mid = online_train(src2, c, w0);
+  std::stringstream s2;
+  save_checkpoint(s2, mid);
+  OnlineState back2 = load_checkpoint(s2);
+  c.max_epochs_or_samples = 2 * N;
+  online_resume(back2, src2, c);
+  CHECK(back2.t == full.t && back2.commits == full.commits);
+  double worst = 0.0;
+  for (Index i = 0; i < F * K; ++i)
+    worst = std::max(worst, std::abs(back2.dict.w.data()[i] - full.dict.w.data()[i]) / full.dict.w.data()[i]);
+  CHECK(worst < 1e-5);
+}
+
+TEST_CASE("evaluate_heldout: frozen W, deterministic, errors (harness.hpp:17-37)") {
+  const Index F = 33, K = 3, N = 40;
+  Matrix v = spectrogram(F, K, N, 41);
+  Matrix w = normalized(random_positive(F, K, 42, 0.1, 1.0));
+  const Matrix w_copy = w;
+  const double d1 = evaluate_heldout(w, v, 1e-12);
+  const double d2 = evaluate_heldout(w, v, 1e-12);
+  CHECK(d1 == d2 && d1 > 0.0 && std::isfinite(d1));
+  CHECK(std::memcmp(w.data(), w_copy.data(), size_t(F * K) * sizeof(double)) == 0);
+  CHECK(evaluate_heldout(w, v, 1e-12, 100, 7) != d1);           // the seed picks the random init
+  CHECK(evaluate_heldout(w, v, 1e-12, 200) <= d1 * (1 + 1e-6));  // more MM iterations never hurt
+  CHECK_THROWS_AS(evaluate_heldout(w, Matrix::Ones(F + 1, 4), 1e-12), ShapeMismatch);
+  CHECK_THROWS_AS(evaluate_heldout(w, Matrix(F, 0), 1e-12), EmptyDataset);
+}

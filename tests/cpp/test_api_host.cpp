@@ -147,3 +147,107 @@ TEST_CASE("init_from_samples / default_h0 (batch.hpp:58-78)") {
 }
 
 MT_MAIN()
+
+TEST_CASE("matrix files round-trip bit-exactly and reject bad input (io.hpp)") {
+  Matrix m = random_positive(7, 5, 11);
+  m(3, 2) = 0.0;
+  m(0, 0) = 1e-300;
+  std::stringstream ss;
+  save_matrix(ss, m);
+  CHECK(ss.str().size() == 4 + 4 + 16 + 8 * 35);
+  Matrix r = load_matrix(ss);
+  CHECK(r.rows() == 7 && r.cols() == 5);
+  CHECK(std::memcmp(r.data(), m.data(), 35 * sizeof(double)) == 0);
+  std::stringstream bad("ISNX0000");
+  CHECK_THROWS_AS(load_matrix(bad), BadMagic);
+  std::string s = ss.str();
+  std::stringstream trunc(s.substr(0, s.size() - 3));
+  CHECK_THROWS_AS(load_matrix(trunc), TruncatedPayload);
+  Matrix neg = m;
+  neg(1, 1) = -1.0;
+  std::stringstream sn;
+  save_matrix(sn, neg);
+  CHECK_THROWS_AS(load_matrix(sn), NegativeEntry);
+}
+
+TEST_CASE("checkpoints round-trip every field bit-exactly (online.hpp:421-489)") {
+  for (RestartMode mode : {RestartMode::warm, RestartMode::fresh}) {
+    OnlineState st;
+    st.dict.w = random_positive(9, 3, 1);
+    st.dict.a = random_positive(9, 3, 2);
+    st.dict.b = random_positive(9, 3, 3);
+    st.pending_a = random_positive(9, 3, 4);
+    st.pending_b = random_positive(9, 3, 5);
+    if (mode == RestartMode::warm) st.warm_h = random_positive(3, 11, 6);
+    st.restart = mode;
+    st.t = 123456789012ULL;
+    st.seed = 0xdeadbeefULL;
+    st.commits = 77;
+    st.rho = 0.95967;
+    std::stringstream ss;
+    save_checkpoint(ss, st);
+    OnlineState r = load_checkpoint(ss);
+    CHECK(r.restart == mode && r.t == st.t && r.seed == st.seed && r.commits == st.commits);
+    CHECK(std::memcmp(&r.rho, &st.rho, 8) == 0);
+    const Matrix* a[] = {&st.dict.w, &st.dict.a, &st.dict.b, &st.pending_a, &st.pending_b, &st.warm_h};
+    const Matrix* b[] = {&r.dict.w, &r.dict.a, &r.dict.b, &r.pending_a, &r.pending_b, &r.warm_h};
+    for (int i = 0; i < 6; ++i) {
+      CHECK(a[i]->rows() == b[i]->rows() && a[i]->cols() == b[i]->cols());
+      CHECK(std::memcmp(a[i]->data(), b[i]->data(), size_t(a[i]->size()) * sizeof(double)) == 0);
+    }
+  }
+  std::stringstream bad("ISCX");
+  CHECK_THROWS_AS(load_checkpoint(bad), BadMagic);
+  std::stringstream mode;
+  mode.write("ISCK", 4);
+  const unsigned char v1[4] = {1, 0, 0, 0}, m7[4] = {7, 0, 0, 0};
+  mode.write(reinterpret_cast<const char*>(v1), 4);
+  mode.write(reinterpret_cast<const char*>(m7), 4);
+  CHECK_THROWS_AS(load_checkpoint(mode), UnsupportedFormat);
+}
+
+TEST_CASE("ChunkStreamSource: next() and the next_block fast path agree across chunks and buffers") {
+  const Index F = 3;
+  std::string bytes;
+  auto put64 = [&](std::uint64_t v) {
+    for (int i = 0; i < 8; ++i) bytes.push_back(char((v >> (8 * i)) & 0xff));
+  };
+  double val = 0.0;
+  for (std::uint64_t count : {5u, 0u, 7u, 2u}) {  // 14 frames in ragged chunks (one empty)
+    put64(count);
+    for (std::uint64_t c = 0; c < count * std::uint64_t(F); ++c) {
+      val += 1.0;
+      std::uint64_t b;
+      std::memcpy(&b, &val, 8);
+      put64(b);
+    }
+  }
+  std::istringstream in1(bytes), in2(bytes);
+  ChunkStreamSource a(in1, F, 4, 9), b(in2, F, 4, 9);
+  std::vector<double> seq;
+  std::vector<std::uint64_t> idx;
+  while (auto s = a.next()) {
+    for (Index f = 0; f < F; ++f) seq.push_back(s->frame[f]);
+    idx.push_back(s->index);
+  }
+  CHECK(seq.size() == 14 * 3);
+  std::vector<float> blk(14 * 3);
+  std::vector<std::uint64_t> bidx(14);
+  std::size_t got = b.next_block(5, F, blk.data(), bidx.data());
+  got += b.next_block(20, F, blk.data() + got * 3, bidx.data() + got);
+  CHECK(got == 14);
+  for (std::size_t i = 0; i < seq.size(); ++i) CHECK(blk[i] == float(seq[i]));
+  for (std::size_t i = 0; i < 14; ++i) CHECK(bidx[i] == i && idx[i] == i);
+  // within each 4-frame buffer the frames are the reference's permutation of arrival order
+  for (std::size_t blk0 = 0; blk0 < 14; blk0 += 4) {
+    const std::size_t len = std::min<std::size_t>(4, 14 - blk0);
+    const auto perm = detail::shuffled_range(len, 9, blk0 / 4);
+    for (std::size_t i = 0; i < len; ++i) CHECK(seq[(blk0 + i) * 3] == double(3 * (blk0 + perm[i]) + 1));
+  }
+  std::string bad = bytes;
+  bad[8 + 8 * 4] = 0;
+  bad[8 + 8 * 4 + 7] = char(0xff);  // frame 1, bin 1 becomes negative / non-finite
+  std::istringstream in3(bad);
+  ChunkStreamSource c(in3, F, 4, 9);
+  CHECK_THROWS_AS(c.next(), NonFiniteEntry);
+}

@@ -131,3 +131,20 @@ def test_cycle_permutation_is_a_permutation():  # online.hpp:79-87
     assert sorted(p.tolist()) == list(range(100))
     assert not np.array_equal(p, O.cycle_permutation(3, 1, 100))
     assert np.array_equal(p, O.cycle_permutation(3, 0, 100))
+
+
+def test_heldout_init_stream_and_objective():  # harness.hpp:17-37
+    rng = np.random.default_rng(5)
+    w = rng.uniform(0.1, 1.0, (33, 4))
+    w /= w.sum(axis=0)
+    t = rng.uniform(0.01, 2.0, (33, 20))
+    h0 = O.heldout_h0(w, t, 1e-12, 0x45)
+    u = O.uniform01(O.mix_seed(0x45, 0xE7A1), 4 * 20)  # one stream, column-major fill
+    scale = max(t.mean(), 1e-12) / (4 * w.mean())
+    assert np.allclose(h0, scale * (1.0 - u).reshape(20, 4).T, rtol=1e-13, atol=0)
+    d0 = O.evaluate_heldout(w, t, 1e-12, 0, 0x45)
+    assert abs(d0 - O.objective(t, w, h0, 1e-12)) <= 1e-12 * d0
+    d = [O.evaluate_heldout(w, t, 1e-12, it, 0x45) for it in (1, 10, 100)]
+    assert d0 > d[0] > d[1] > d[2] > 0.0
+    with pytest.raises(O.OracleError):
+        O.evaluate_heldout(w, t[:5], 1e-12)
