@@ -44,7 +44,7 @@ MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FP32_PEAK_FALLBACK = 72.4  # TFLOP/s, tools/probe measured on this pool (profiles/r01_probe.txt)
 
 
-def parse():
+def parse(argv=None):
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=3)
@@ -55,7 +55,10 @@ def parse():
     p.add_argument("--cpu-sample-batches", type=int, default=4)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
-    return p.parse_args()
+    return p.parse_args(argv)
+
+
+parse_args = parse
 
 
 class ClockSampler:
@@ -100,19 +103,34 @@ class ClockSampler:
                 "samples": len(self.rows), "reasons": reasons}
 
 
+_BACKEND = None
+
+
 def dist_init():
+    """One process per GPU (torchrun env).  Replicas only: the collectives are a
+    barrier and the max-over-ranks of the timed region, over NCCL on GPU boxes
+    (gloo on CPU, or BENCH_DIST_BACKEND)."""
+    global _BACKEND
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if world > 1:
+        import torch
         import torch.distributed as dist
-        dist.init_process_group("gloo")
+        _BACKEND = os.environ.get("BENCH_DIST_BACKEND") or ("nccl" if torch.cuda.is_available() else "gloo")
+        if _BACKEND == "nccl":
+            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)) % torch.cuda.device_count())
+        dist.init_process_group(_BACKEND)
     return rank, world
 
 
 def barrier(world):
     if world > 1:
+        import torch
         import torch.distributed as dist
-        dist.barrier()
+        if _BACKEND == "nccl":
+            dist.barrier(device_ids=[torch.cuda.current_device()])
+        else:
+            dist.barrier()
 
 
 def allmax(x, world):
@@ -120,9 +138,15 @@ def allmax(x, world):
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64)
+    t = torch.tensor([x], dtype=torch.float64, device="cuda" if _BACKEND == "nccl" else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def dist_done(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
 
 
 def roofline_peak():
@@ -203,6 +227,7 @@ def run_batch(args, rank, world):
 
     import paper_1106_4198_b200 as E
     from tools.synth import spectrogram_torch
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)) % max(torch.cuda.device_count(), 1))
     cfg = dict(CONFIGS["c2"])
     F, K, N = cfg["F"], cfg["K"], args.frames or cfg["N"]
     epochs = cfg["epochs"]
@@ -215,19 +240,21 @@ def run_batch(args, rank, world):
     torch.cuda.synchronize()
     times = []
     for _ in range(args.steps):
+        barrier(world)
         t0 = time.perf_counter()
         out = E.batch_train(vd, w0, h0, epochs)
         torch.cuda.synchronize()
-        times.append(time.perf_counter() - t0)
+        times.append(allmax(time.perf_counter() - t0, world))
     t = float(np.median(times))
     flops = 12.0 * F * K * N * epochs + 2.0 * F * K * N
     if rank == 0:
-        print(json.dumps({"metric": "batch IS-NMF epochs/sec (F=513,K=50,N=225k)", "value": epochs / t,
+        print(json.dumps({"metric": "batch IS-NMF epochs/sec (F=513,K=50,N=225k)", "value": world * epochs / t,
                           "unit": "epochs/s", "n_gpus": world, "steps": args.steps, "warmup": 1,
                           "ms_per_step": 1e3 * t, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
                           "dtype": "f32", "data": "synthetic",
                           "config": {"workload": f"c2: F={F}, K={K}, N={N}, {epochs} epochs (host-timed, includes "
-                                                 f"H upload/download)", "parallelism": "single"},
+                                                 f"H upload/download)",
+                                     "parallelism": "replicas" if world > 1 else "single"},
                           "achieved_tflops": flops / t / 1e12, "final_obj": float(out["obj"][-1]),
                           "initial_obj": out["initial_obj"]}), flush=True)
 
@@ -373,6 +400,7 @@ def main():
         run_batch(args, rank, world)
     else:
         run_engine(args, rank, world)
+    dist_done(world)
 
 
 if __name__ == "__main__":
