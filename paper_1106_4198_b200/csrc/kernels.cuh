@@ -256,12 +256,14 @@ __device__ __forceinline__ void load_v(float (&vv)[4][TN], const float* const* f
 // vt = V of cell `lane` when rows * NT <= 32 (loaded once per launch).
 template <int TK, int TN>
 __device__ __forceinline__ void phase_a(const float* Ws, const float* Hs, float* QR, const float* const* fptr,
-                                        int c0, int rows, int nf, float eps, int lane, const float (&vv)[4][TN],
-                                        float vt) {
+                                        int c0, int rows, int nf, float eps, int lane, float vt) {
   using S = SolveShape<TK, TN>;
   constexpr int KP = S::KP, NT = S::NT, WS = S::WS;
   if (rows == kChunk) {
     const int rg = pa_rg(lane), fg = pa_fg(lane);  // 8 row groups x 4 frame groups
+    // V of this lane's cells (an L2 hit after the first pass), in flight during the k loop
+    float vv[4][TN];
+    load_v<TN>(vv, fptr, c0, nf, lane);
     float acc[4][TN];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
@@ -462,9 +464,6 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(const SolveArgs a) {
   const int r0 = (warp * F) / kWarps, r1 = ((warp + 1) * F) / kWarps;
   // full 32-row chunks of this warp, visited cyclically; V is prefetched one ahead
   const int nfull = (r1 - r0) / kChunk;
-  auto next_full = [&](int c0) { return (c0 + kChunk < r0 + nfull * kChunk) ? c0 + kChunk : r0; };
-  float vv[4][TN];
-  if (nfull > 0) load_v<TN>(vv, fptr, r0, nf, lane);
   // V of the tail chunk's cell `lane` (constant over the passes)
   float vt = 0.0f;
   {
@@ -489,8 +488,7 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(const SolveArgs a) {
 
     for (int c0 = r0; c0 < r1; c0 += kChunk) {
       const int rows = min(kChunk, r1 - c0);
-      phase_a<TK, TN>(Ws, Hs, QR, fptr, c0, rows, nf, eps, lane, vv, vt);
-      if (rows == kChunk) load_v<TN>(vv, fptr, next_full(c0), nf, lane);
+      phase_a<TK, TN>(Ws, Hs, QR, fptr, c0, rows, nf, eps, lane, vt);
       __syncwarp();
       if (a.div_first && pass == 0) divacc += chunk_divergence<TN>(QR, rows, nf, lane);
       PROF_MARK(1);  // phase A
@@ -557,8 +555,7 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(const SolveArgs a) {
     const int rgs = lane & 7, kgs = lane >> 3;
     for (int c0 = r0; c0 < r1; c0 += kChunk) {
       const int rows = min(kChunk, r1 - c0);
-      phase_a<TK, TN>(Ws, Hs, QR, fptr, c0, rows, nf, eps, lane, vv, vt);
-      if (rows == kChunk) load_v<TN>(vv, fptr, next_full(c0), nf, lane);
+      phase_a<TK, TN>(Ws, Hs, QR, fptr, c0, rows, nf, eps, lane, vt);
       __syncwarp();
       if (want_div) divacc += chunk_divergence<TN>(QR, rows, nf, lane);
       PROF_MARK(5);  // stats pass phase A + divergence
