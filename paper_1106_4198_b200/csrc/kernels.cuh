@@ -529,9 +529,13 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(const SolveArgs a) {
         for (int t = 0; t < TN; ++t) pb[j * TN + t] = accB[j][t];
     }
     __syncthreads();
-    for (int p = tid; p < K * NT; p += kThreads) {
+    // compile-time trip count: every thread's loads of all its items are independent
+    constexpr int MI = (KP * NT + kThreads - 1) / kThreads;
+#pragma unroll
+    for (int m = 0; m < MI; ++m) {
+      const int p = tid + m * kThreads;
       const int k = p / NT, n = p - k * NT;  // NT is a compile-time constant
-      if (n < nf) {
+      if (k < K && n < nf) {
         int kgp, jp;
         KM::inv(k, kgp, jp);
         const int ngp = n / TN, tp = n - ngp * TN;
