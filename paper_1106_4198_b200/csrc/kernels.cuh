@@ -183,8 +183,41 @@ struct SolveShape {
   static constexpr int PBS = (cells % 2 == 1) ? cells : cells + 1;
   static constexpr int union_floats =
       (kWarps * kChunk * kQS > kWarps * 32 * PBS) ? kWarps * kChunk * kQS : kWarps * 32 * PBS;
-  static size_t smem_bytes(int F) { return sizeof(float) * (size_t(F) * WS + NT * KP + union_floats); }
+  // phase A on the tensor pipe (3xTF32 mma.sync m16n8k8, Lam^T = h^T W^T):
+  // frames are the M dimension (MB blocks of 16), k the K dimension (KB blocks of 8)
+  static constexpr int MB = (NT + 15) / 16;
+  static constexpr int KB = (KP + 7) / 8;
+  static constexpr int HF = MB * KB * 32 * 4;  // A fragments of h (one of hi / lo)
+  static size_t smem_bytes(int F) { return sizeof(float) * (size_t(F) * WS + NT * KP + 2 * HF + union_floats); }
 };
+
+// Position of h[k][n] in the A-fragment copy (m16n8k8 tf32, row-major A = h^T):
+// thread (g, t) of block (mb, kb) holds A[g][t], A[g+8][t], A[g][t+4], A[g+8][t+4].
+template <int KB>
+__device__ __forceinline__ int hfrag_index(int n, int k) {
+  const int mb = n >> 4, r = n & 15, kb = k >> 3, c = k & 7;
+  const int lane = 4 * (r & 7) + (c & 3), e = (r >> 3) + 2 * (c >> 2);
+  return ((mb * KB + kb) * 32 + lane) * 4 + e;
+}
+
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+// h -> the hi / lo fragment copies (hi = tf32(h), lo = h - hi)
+__device__ __forceinline__ void put_hfrag(float* Hhi, float* Hlo, int idx, float h) {
+  const float hi = tf32_rna(h);
+  Hhi[idx] = hi;
+  Hlo[idx] = h - hi;
+}
+
+__device__ __forceinline__ void mma_tf32(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
 
 // Loads the lane's TK dictionary values of one row (k-set of group kg).
 template <int TK>
@@ -349,6 +382,132 @@ __device__ __forceinline__ void phase_a(const float* Ws, const float* Hs, float*
   }
 }
 
+// Phase A of a full 32-row chunk on the tensor pipe: Lam^T (frames x rows) =
+// h^T W^T + eps in 3xTF32 (lo*hi + hi*lo + hi*hi, fp32 accumulate: ~1e-6
+// relative), then q = (v+eps)/Lam^2 and r = 1/Lam staged as in phase_a.
+// A = h^T from the fragment copies (one LDS.128 per block), B = W^T read
+// straight from the row-major dictionary (b0 = W[row g][8kb+t], b1 = ..+4);
+// hi = the raw fp32 bits (the tensor core reads the tf32 part), lo = x minus
+// its tf32 truncation.  C: c0/c1 = (frame g, rows 2t, 2t+1), c2/c3 = frame g+8.
+// The work is split in steps (one k block each) so phase B of the previous
+// chunk can interleave them: the HMMA pipe runs beside the FFMA pipe.
+template <int TK, int TN>
+struct MmaA {
+  using S = SolveShape<TK, TN>;
+  static constexpr int KP = S::KP, NT = S::NT, WS = S::WS, MB = S::MB, KB = S::KB;
+  float acc[MB][4][4];
+  uint32_t ahi[MB][4], alo[MB][4], bh[4][2], bl[4][2];  // operands of the current k block
+
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+      for (int nb = 0; nb < 4; ++nb)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[mb][nb][e] = 0.0f;
+  }
+  // operands of k block kb: A fragments (hi, lo) and W (raw = hi, remainder = lo)
+  __device__ __forceinline__ void load(const float* Ws, const float* Hhi, const float* Hlo, int c0, int kb,
+                                       int lane) {
+    const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+    for (int mb = 0; mb < MB; ++mb) {
+      const float4 x = *reinterpret_cast<const float4*>(Hhi + ((mb * KB + kb) * 32 + lane) * 4);
+      const float4 y = *reinterpret_cast<const float4*>(Hlo + ((mb * KB + kb) * 32 + lane) * 4);
+      ahi[mb][0] = __float_as_uint(x.x);
+      ahi[mb][1] = __float_as_uint(x.y);
+      ahi[mb][2] = __float_as_uint(x.z);
+      ahi[mb][3] = __float_as_uint(x.w);
+      alo[mb][0] = __float_as_uint(y.x);
+      alo[mb][1] = __float_as_uint(y.y);
+      alo[mb][2] = __float_as_uint(y.z);
+      alo[mb][3] = __float_as_uint(y.w);
+    }
+    const float* wrow = Ws + (c0 + g) * WS + t + 8 * kb;
+#pragma unroll
+    for (int nb = 0; nb < 4; ++nb) {
+      const float w0 = wrow[8 * nb * WS];
+      const float w1 = (KP % 8 == 0 || kb + 1 < KB) ? wrow[8 * nb * WS + 4] : 0.0f;  // k >= KP reads nothing
+      bh[nb][0] = __float_as_uint(w0);
+      bh[nb][1] = __float_as_uint(w1);
+      bl[nb][0] = __float_as_uint(w0 - __uint_as_float(__float_as_uint(w0) & 0xffffe000u));
+      bl[nb][1] = __float_as_uint(w1 - __uint_as_float(__float_as_uint(w1) & 0xffffe000u));
+    }
+  }
+  // one of the three products (0: lo*hi, 1: hi*lo, 2: hi*hi) for every (mb, nb) block
+  __device__ __forceinline__ void sweep(int s) {
+#pragma unroll
+    for (int nb = 0; nb < 4; ++nb)
+#pragma unroll
+      for (int mb = 0; mb < MB; ++mb) {
+        if (s == 0) mma_tf32(acc[mb][nb], alo[mb], bh[nb][0], bh[nb][1]);
+        if (s == 1) mma_tf32(acc[mb][nb], ahi[mb], bl[nb][0], bl[nb][1]);
+        if (s == 2) mma_tf32(acc[mb][nb], ahi[mb], bh[nb][0], bh[nb][1]);
+      }
+  }
+  __device__ __forceinline__ void step(const float* Ws, const float* Hhi, const float* Hlo, int c0, int kb,
+                                       int lane) {
+    load(Ws, Hhi, Hlo, c0, kb, lane);
+    sweep(0);
+    sweep(1);
+    sweep(2);
+  }
+  // V of this lane's output cells (frames g + 8*h8 + 16*mb, rows 8nb + 2t + e)
+  static __device__ __forceinline__ void load_v(float (&v)[MB][2][4][2], const float* const* fptr, int c0, int nf,
+                                                int lane) {
+    const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+    for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+      for (int h8 = 0; h8 < 2; ++h8) {
+        const int n = 16 * mb + g + 8 * h8;
+        const bool valid = n < nf;
+        const float* vp = fptr[valid ? n : 0] + c0 + 2 * t;
+#pragma unroll
+        for (int nb = 0; nb < 4; ++nb) {
+          v[mb][h8][nb][0] = valid ? __ldg(vp + 8 * nb) : 0.0f;
+          v[mb][h8][nb][1] = valid ? __ldg(vp + 8 * nb + 1) : 0.0f;
+        }
+      }
+  }
+  // q, r of the chunk into QR
+  __device__ __forceinline__ void finish(const float (&v)[MB][2][4][2], float* QR, int nf, float eps,
+                                         int lane) const {
+    const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+    for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+      for (int h8 = 0; h8 < 2; ++h8) {
+        const int n = 16 * mb + g + 8 * h8;
+        if (n >= NT) continue;
+        const bool valid = n < nf;
+        float* qp = QR + 2 * t * kQS + (n / TN) * 8 + (n % TN);
+#pragma unroll
+        for (int nb = 0; nb < 4; ++nb)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const float r = rcp_approx(acc[mb][nb][2 * h8 + e] + eps);
+            const float q = (v[mb][h8][nb][e] + eps) * r * r;
+            qp[(8 * nb + e) * kQS] = valid ? q : 0.0f;
+            qp[(8 * nb + e) * kQS + kQR_R] = valid ? r : 0.0f;
+          }
+      }
+  }
+};
+
+template <int TK, int TN>
+__device__ __forceinline__ void phase_a_mma(const float* Ws, const float* Hhi, const float* Hlo, float* QR,
+                                            const float* const* fptr, int c0, int nf, float eps, int lane) {
+  using M = MmaA<TK, TN>;
+  M m;
+  float v[M::MB][2][4][2];
+  M::load_v(v, fptr, c0, nf, lane);  // in flight during the k loop
+  m.zero();
+#pragma unroll 1
+  for (int kb = 0; kb < M::KB; ++kb) m.step(Ws, Hhi, Hlo, c0, kb, lane);
+  m.finish(v, QR, nf, eps, lane);
+}
+
 // IS divergence of the staged chunk (online.hpp:303-309 / kernels.hpp:52-53):
 // 1 + u = (v+eps)/lam = q / r, branch-free, four independent partial sums.
 template <int TN>
@@ -378,7 +537,9 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(const SolveArgs a) {
   const int F = a.F, K = a.K;
   float* Ws = smem;           // [F][WS]
   float* Hs = Ws + F * WS;    // [NT][KP]
-  float* UN = Hs + NT * KP;   // union: per-warp Q/R staging | per-lane num/den partials
+  float* Hhi = Hs + NT * KP;  // h^T A-fragments for the tensor-pipe phase A: tf32 hi
+  float* Hlo = Hhi + S::HF;   //   and the fp32 remainder
+  float* UN = Hlo + S::HF;    // union: per-warp Q/R staging | per-lane num/den partials
   __shared__ const float* fptr[NT];
   __shared__ double red[kWarps];
   __shared__ double meanv[NT];
@@ -423,7 +584,9 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(const SolveArgs a) {
     __syncthreads();
   }
 
-  // h0 -> Hs
+  for (int i = tid; i < 2 * S::HF; i += kThreads) Hhi[i] = 0.0f;  // padding frames / k stay 0
+  __syncthreads();
+  // h0 -> Hs (+ fragment copies)
   for (int idx = tid; idx < NT * KP; idx += kThreads) {
     const int n = idx / KP, k = idx - n * KP;
     float val = 0.0f;
@@ -443,6 +606,7 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(const SolveArgs a) {
       if (a.check_h0 && !(val > 0.0f)) s_bad = 1;
     }
     Hs[idx] = val;
+    put_hfrag(Hhi, Hlo, hfrag_index<S::KB>(n, k), val);
   }
   {  // wait for the dictionary (phase 0 of wbar)
     const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&wbar));
@@ -486,33 +650,74 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(const SolveArgs a) {
 #pragma unroll
       for (int t = 0; t < TN; ++t) accB[j][t] = 0.0f;
 
+    // chunk 0's phase A runs alone; phase A of every further full chunk runs
+    // on the tensor pipe interleaved with phase B of the chunk before it
+    MmaA<TK, TN> mA;
+    if (nfull > 0) phase_a_mma<TK, TN>(Ws, Hhi, Hlo, QR, fptr, r0, nf, eps, lane);
     for (int c0 = r0; c0 < r1; c0 += kChunk) {
       const int rows = min(kChunk, r1 - c0);
-      phase_a<TK, TN>(Ws, Hs, QR, fptr, c0, rows, nf, eps, lane, vt);
+      if (rows < kChunk) phase_a<TK, TN>(Ws, Hs, QR, fptr, c0, rows, nf, eps, lane, vt);
       __syncwarp();
       if (a.div_first && pass == 0) divacc += chunk_divergence<TN>(QR, rows, nf, lane);
       PROF_MARK(1);  // phase A
-      // ---------------- phase B: num += W^T q, den += W^T r (this warp's rows),
-      // loads of row rl+1 issued before the FMAs of row rl
+      // ---------------- phase B: num += W^T q, den += W^T r (this warp's rows)
       const float* wr = Ws + c0 * WS;
       const float* xr = QR + nd * kQR_R + ng * 8;
-      float w[TK], x[TN];
-      load_wk<TK>(wr, kg, w);
-      load_x<TN>(xr, x);
+      const bool overlap = c0 + kChunk < r0 + nfull * kChunk;  // the next chunk is a full one
+      if (overlap) {
+        // 4 rows of phase B per iteration with one k block of the next chunk's
+        // MMA phase A in the same basic block, so the scheduler can interleave
+        // HMMA with FFMA (in-order issue: a separate HMMA burst would stall the
+        // FFMAs behind it)
+        constexpr int KB = MmaA<TK, TN>::KB;
+        static_assert(KB <= kChunk / 4, "one k block per 4-row step");
+        mA.zero();
+        auto row = [&](int rl) {
+          float w[TK], x[TN];
+          load_wk<TK>(wr + rl * WS, kg, w);
+          load_x<TN>(xr + rl * kQS, x);
+#pragma unroll
+          for (int j = 0; j < TK; ++j)
+#pragma unroll
+            for (int t = 0; t < TN; ++t) accB[j][t] = fmaf(w[j], x[t], accB[j][t]);
+        };
+        // each 4-row step carries one k block: its three MMA sweeps sit between rows
+#pragma unroll 1
+        for (int it = 0; it < KB; ++it) {
+          mA.load(Ws, Hhi, Hlo, c0 + kChunk, it, lane);
+          row(4 * it);
+          mA.sweep(0);
+          row(4 * it + 1);
+          mA.sweep(1);
+          row(4 * it + 2);
+          mA.sweep(2);
+          row(4 * it + 3);
+        }
+        float vn[MmaA<TK, TN>::MB][2][4][2];  // V of the next chunk, in flight under the last rows
+        MmaA<TK, TN>::load_v(vn, fptr, c0 + kChunk, nf, lane);
+#pragma unroll 1
+        for (int rl = 4 * KB; rl < kChunk; ++rl) row(rl);
+        __syncwarp();  // phase B is done with this chunk's Q/R
+        mA.finish(vn, QR, nf, eps, lane);
+      } else {  // loads of row rl+1 issued before the FMAs of row rl
+        float w[TK], x[TN];
+        load_wk<TK>(wr, kg, w);
+        load_x<TN>(xr, x);
 #pragma unroll 2
-      for (int rl = 0; rl < rows; ++rl) {
-        float wn[TK], xn[TN];
-        const int rn = rl + 1 < rows ? rl + 1 : rl;
-        load_wk<TK>(wr + rn * WS, kg, wn);
-        load_x<TN>(xr + rn * kQS, xn);
+        for (int rl = 0; rl < rows; ++rl) {
+          float wn[TK], xn[TN];
+          const int rn = rl + 1 < rows ? rl + 1 : rl;
+          load_wk<TK>(wr + rn * WS, kg, wn);
+          load_x<TN>(xr + rn * kQS, xn);
 #pragma unroll
-        for (int j = 0; j < TK; ++j)
+          for (int j = 0; j < TK; ++j)
 #pragma unroll
-          for (int t = 0; t < TN; ++t) accB[j][t] = fmaf(w[j], x[t], accB[j][t]);
+            for (int t = 0; t < TN; ++t) accB[j][t] = fmaf(w[j], x[t], accB[j][t]);
 #pragma unroll
-        for (int j = 0; j < TK; ++j) w[j] = wn[j];
+          for (int j = 0; j < TK; ++j) w[j] = wn[j];
 #pragma unroll
-        for (int t = 0; t < TN; ++t) x[t] = xn[t];
+          for (int t = 0; t < TN; ++t) x[t] = xn[t];
+        }
       }
       __syncwarp();
       PROF_MARK(2);  // phase B
@@ -548,6 +753,7 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(const SolveArgs a) {
         }
         float& h = Hs[n * KP + k];
         h = h * sqrtf(num / den);
+        put_hfrag(Hhi, Hlo, hfrag_index<S::KB>(n, k), h);
       }
     }
     __syncthreads();
@@ -559,7 +765,10 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(const SolveArgs a) {
     const int rgs = lane & 7, kgs = lane >> 3;
     for (int c0 = r0; c0 < r1; c0 += kChunk) {
       const int rows = min(kChunk, r1 - c0);
-      phase_a<TK, TN>(Ws, Hs, QR, fptr, c0, rows, nf, eps, lane, vt);
+      if (rows == kChunk)
+        phase_a_mma<TK, TN>(Ws, Hhi, Hlo, QR, fptr, c0, nf, eps, lane);
+      else
+        phase_a<TK, TN>(Ws, Hs, QR, fptr, c0, rows, nf, eps, lane, vt);
       __syncwarp();
       if (want_div) divacc += chunk_divergence<TN>(QR, rows, nf, lane);
       PROF_MARK(5);  // stats pass phase A + divergence
