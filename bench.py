@@ -377,7 +377,8 @@ def run_engine(args, rank, world):
                              "frac": achieved / peak, "traffic": k1_traffic(),
                              "traffic_unit": "bytes per launch (ncu dram__bytes_read+write)",
                              "algorithmic_bytes_per_launch": frames_per_launch * (4 * F + 8 * K),
-                             "kernel": "solve_kernel" if K <= 64 else "solve_generic_kernel",
+                             "kernel": ("solve_kernel (FP32 FMA + 3xTF32 mma.sync phase A)" if K <= 64 else
+                                        "solve_large_kernel (3xTF32 mma.sync, tensor pipe)"),
                              "ms_per_launch": k1_ms,
                              "flops_per_launch": flops_per_frame * frames_per_launch,
                              "k1_share_of_step": kstats["solve_ms"] / kstats["span_ms"],

@@ -23,6 +23,7 @@
 
 #include "../../include/isnmf_b200.h"
 #include "kernels.cuh"
+#include "kernels_large.cuh"
 
 using namespace isnmf_dev;
 
@@ -159,7 +160,20 @@ int pick_variant(int64_t F, int64_t K, int64_t frames, Variant** out, int* WS, s
 
 // Solve-kernel choice for (F, K, frames per batch): a register-tiled variant when
 // W fits shared memory, else the generic streaming kernel.
+// Tensor-pipe kernel for 64 < K <= 256 (config 4): [MBW - 1][NB - 1]
+using LargeFn = void (*)(const SolveArgs);
+#define LG(m, n) solve_large_kernel<m, n>
+LargeFn g_large[2][8] = {{LG(1, 1), LG(1, 2), LG(1, 3), LG(1, 4), LG(1, 5), LG(1, 6), LG(1, 7), LG(1, 8)},
+                         {LG(2, 1), LG(2, 2), LG(2, 3), LG(2, 4), LG(2, 5), LG(2, 6), LG(2, 7), LG(2, 8)}};
+#undef LG
+size_t large_smem(int mbw, int nb) {
+  const int KP = 128 * mbw, NT = 8 * nb, FMB = (NT + 15) / 16;
+  return sizeof(float) * (size_t(16 * FMB) * (KP + 4) + 2 * size_t(kLgChunk) * (KP + 4) + size_t(kLgChunk) * 136);
+}
+bool large_configured[2][8] = {};
+
 struct SolvePlan {
+  LargeFn large = nullptr;  // tensor-pipe kernel for large K
   Variant* var = nullptr;  // nullptr: generic
   int NT = 0, KP = 0, WS = 0;
   size_t smem = 0;
@@ -182,6 +196,25 @@ int plan_solve(int64_t F, int64_t K, int64_t frames, SolvePlan* plan, bool force
   }
   if (rc != 1) return rc;
   const int64_t per_cta = (frames + device_sms() - 1) / device_sms();
+  if (!force_generic && K > 64 && K <= 256) {
+    const int nb = int(std::min<int64_t>(8, std::max<int64_t>(1, (per_cta + 7) / 8)));
+    const int mbw = K <= 128 ? 1 : 2;
+    const size_t smem = large_smem(mbw, nb);
+    if (smem + 2048 <= size_t(smem_optin())) {
+      if (!large_configured[mbw - 1][nb - 1]) {
+        CU(cudaFuncSetAttribute(g_large[mbw - 1][nb - 1], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                smem_optin() - 2048));
+        large_configured[mbw - 1][nb - 1] = true;
+      }
+      plan->large = g_large[mbw - 1][nb - 1];
+      plan->var = nullptr;
+      plan->NT = 8 * nb;
+      plan->KP = 128 * mbw;
+      plan->WS = ws_for(128 * mbw);
+      plan->smem = smem;
+      return 0;
+    }
+  }
   int nt = int(std::min<int64_t>(64, std::max<int64_t>(1, per_cta)));
   while (nt > 1 && K * nt > int64_t(kGenThreads) * kGenMaxPairs) --nt;
   if (K * nt > int64_t(kGenThreads) * kGenMaxPairs)
@@ -203,7 +236,9 @@ int plan_solve(int64_t F, int64_t K, int64_t frames, SolvePlan* plan, bool force
 }
 
 void launch_solve(const SolvePlan& p, int nblk, const SolveArgs& a, cudaStream_t s) {
-  if (p.var)
+  if (p.large)
+    p.large<<<nblk, kLgThreads, p.smem, s>>>(a);
+  else if (p.var)
     p.var->fn<<<nblk, kThreads, p.smem, s>>>(a);
   else
     solve_generic_kernel<<<nblk, kGenThreads, p.smem, s>>>(a, p.NT);

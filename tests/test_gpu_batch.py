@@ -18,7 +18,8 @@ def rel(a, b):
     return float(np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-300)))
 
 
-@pytest.mark.parametrize("F,K,N,epochs", [(513, 50, 2000, 5), (257, 10, 3000, 12), (40, 3, 77, 20)])
+@pytest.mark.parametrize("F,K,N,epochs", [(513, 50, 2000, 5), (257, 10, 3000, 12), (40, 3, 77, 20),
+                                          (129, 96, 1500, 4)])  # K = 96: tensor-pipe kernel
 def test_batch_matches_oracle(F, K, N, epochs):
     v = spectrogram_np(F, K, N, seed=21)
     rng = np.random.default_rng(22)

@@ -208,3 +208,33 @@ def test_generic_and_tiled_kernels_agree():
     s1, s2 = e1.state(), e2.state()
     for k in ("w", "a", "b"):
         assert rel(s1[k], s2[k]) < 1e-5
+
+
+@pytest.mark.parametrize("F,K,beta,iters,N,restart", [
+    (1025, 256, 256, 8, 512, "warm"),   # config-4 dictionary shape, 8 frames per CTA
+    (129, 80, 96, 4, 300, "fresh"),     # K <= 128: one m-block per warp
+    (129, 256, 8192, 2, 8192, "warm"),  # config-4 frames per CTA (56), ragged last window
+    (1025, 200, 2048, 3, 2048, "fresh"),  # K padded to 256
+])
+def test_large_k_tensor_kernel(F, K, beta, iters, N, restart):
+    """The tensor-pipe kernel (3xTF32 mma.sync, 64 < K <= 256) against the oracle."""
+    eng, orc, v = make_pair(F, K, beta, iters, N, restart=restart, rho=0.9)
+    orc.run(v.astype(np.float64))
+    eng.run(v)
+    keys = ("w", "a", "b", "pending_a", "pending_b") + (("warm_h",) if restart == "warm" else ())
+    se, so = eng.state(warm_h=restart == "warm"), orc.state(warm_h=restart == "warm")
+    for k in keys:
+        assert rel(se[k], so[k]) < RTOL, (k, rel(se[k], so[k]))
+    assert se["commits"] == so["commits"] and se["pending_count"] == so["pending_count"]
+    assert rel(se["last_minibatch_obj"], so["last_minibatch_obj"]) < RTOL
+
+
+def test_large_k_tensor_and_generic_kernels_agree():
+    F, K, beta, iters, N = 257, 128, 512, 4, 1024
+    e1, _, v = make_pair(F, K, beta, iters, N)
+    e2, _, _ = make_pair(F, K, beta, iters, N, v=v, generic=True)
+    e1.run(v)
+    e2.run(v)
+    s1, s2 = e1.state(), e2.state()
+    for k in ("w", "a", "b"):
+        assert rel(s1[k], s2[k]) < 1e-5
