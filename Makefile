@@ -5,7 +5,7 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v --expt-r
 PKG := paper_1106_4198_b200
 LIB := $(PKG)/lib/libisnmf_b200.so
 SRC := $(PKG)/csrc/engine.cu
-DEPS := $(PKG)/csrc/kernels.cuh include/isnmf_b200.h
+DEPS := $(wildcard $(PKG)/csrc/*.cuh) include/isnmf_b200.h
 
 all: $(LIB) oracle
 

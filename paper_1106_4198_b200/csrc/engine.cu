@@ -173,7 +173,8 @@ size_t large_smem(int mbw, int nb) {
 bool large_configured[2][8] = {};
 
 struct SolvePlan {
-  LargeFn large = nullptr;  // tensor-pipe kernel for large K
+  LargeFn large = nullptr;  // tensor-pipe kernels (large K, or the resident-dictionary variant)
+  int threads = 0;          // block size of `large`
   Variant* var = nullptr;  // nullptr: generic
   int NT = 0, KP = 0, WS = 0;
   size_t smem = 0;
@@ -207,6 +208,7 @@ int plan_solve(int64_t F, int64_t K, int64_t frames, SolvePlan* plan, bool force
         large_configured[mbw - 1][nb - 1] = true;
       }
       plan->large = g_large[mbw - 1][nb - 1];
+      plan->threads = kLgThreads;
       plan->var = nullptr;
       plan->NT = 8 * nb;
       plan->KP = 128 * mbw;
@@ -237,7 +239,7 @@ int plan_solve(int64_t F, int64_t K, int64_t frames, SolvePlan* plan, bool force
 
 void launch_solve(const SolvePlan& p, int nblk, const SolveArgs& a, cudaStream_t s) {
   if (p.large)
-    p.large<<<nblk, kLgThreads, p.smem, s>>>(a);
+    p.large<<<nblk, p.threads, p.smem, s>>>(a);
   else if (p.var)
     p.var->fn<<<nblk, kThreads, p.smem, s>>>(a);
   else
