@@ -151,6 +151,15 @@ __global__ void __launch_bounds__(kLgThreads, 1) solve_large_kernel(const SolveA
 #pragma unroll
             for (int e = 0; e < 4; ++e) acc[i][p][e] = 0.0f;
         const int fmb = min(tile0, 4 * FMB - 1) / 4;  // the warp's tiles share one frame block
+        // V of the outputs (L2 / HBM), in flight during the k loop
+        float vv[TPW][4];
+#pragma unroll
+        for (int i = 0; i < TPW; ++i)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int n = 16 * fmb + g + 8 * (e >> 1), row = 8 * ((tile0 + i) & 3) + 2 * t + (e & 1);
+            vv[i][e] = (tile0 + i < 4 * FMB && n < nf && row < rows) ? __ldg(fptr[n] + c0 + row) : 0.0f;
+          }
         const float* hrow = Hs + (16 * fmb + g) * KPS + t;
 #pragma unroll 1
         for (int kb = 0; kb < KB; kb += 2) {
@@ -186,7 +195,7 @@ __global__ void __launch_bounds__(kLgThreads, 1) solve_large_kernel(const SolveA
           for (int e = 0; e < 4; ++e) {
             const int n = 16 * fmb + g + 8 * (e >> 1), row = 8 * rnb + 2 * t + (e & 1);
             const bool valid = n < nf && row < rows;
-            const float v = valid ? __ldg(fptr[n] + c0 + row) : 0.0f;
+            const float v = vv[i][e];
             const float r = rcp_approx(acc[i][0][e] + acc[i][1][e] + eps);
             const float vpe = v + eps;
             if (want_div && valid) divacc += is_term_ratio(vpe * r);
