@@ -166,10 +166,12 @@ using LargeFn = void (*)(const SolveArgs);
 LargeFn g_large[2][8] = {{LG(1, 1), LG(1, 2), LG(1, 3), LG(1, 4), LG(1, 5), LG(1, 6), LG(1, 7), LG(1, 8)},
                          {LG(2, 1), LG(2, 2), LG(2, 3), LG(2, 4), LG(2, 5), LG(2, 6), LG(2, 7), LG(2, 8)}};
 #undef LG
-size_t large_smem(int mbw, int nb) {
+size_t large_smem(int mbw, int nb) {  // = LargeShape<mbw, nb>::smem_bytes()
   const int KP = 128 * mbw, NT = 8 * nb, FMB = (NT + 15) / 16;
-  return sizeof(float) * (size_t(16 * FMB) * (KP + 4) + 2 * size_t(kLgChunk) * (KP + 4) + size_t(kLgChunk) * 136);
+  return sizeof(float) * (size_t(16 * FMB) * (KP + 4) + 3 * size_t(kLgChunk) * (KP + 4) + 2 * size_t(kLgChunk) * 136);
 }
+static_assert(LargeShape<2, 7>::smem_bytes() == sizeof(float) * (64 * 260 + 3 * 32 * 260 + 2 * 32 * 136),
+              "large_smem() mirrors LargeShape::smem_bytes()");
 bool large_configured[2][8] = {};
 
 struct SolvePlan {

@@ -33,8 +33,8 @@ struct LargeShape {
   static constexpr int WS = KP + 4;          // dictionary row stride (the global W32 layout)
   static constexpr int QRS = 136;            // staging row: q frames [0,64), r [64,128); = 8 mod 32
   static constexpr int HROWS = 16 * FMB;
-  static size_t smem_bytes() {
-    return sizeof(float) * (size_t(HROWS) * KPS + 2 * size_t(kLgChunk) * WS + size_t(kLgChunk) * QRS);
+  static constexpr size_t smem_bytes() {
+    return sizeof(float) * (size_t(HROWS) * KPS + 3 * size_t(kLgChunk) * WS + 2 * size_t(kLgChunk) * QRS);
   }
 };
 
@@ -56,8 +56,8 @@ __global__ void __launch_bounds__(kLgThreads, 1) solve_large_kernel(const SolveA
   if (*a.status || (a.halt && *a.halt)) return;
   extern __shared__ __align__(16) float smem[];
   float* Hs = smem;                   // [HROWS][KPS], zero outside (n < nf, k < K)
-  float* Wb = Hs + HROWS * KPS;       // [2][32][WS]
-  float* QR = Wb + 2 * kLgChunk * WS; // [32][QRS]
+  float* Wb = Hs + HROWS * KPS;        // [3][32][WS]: windows c, c+1 in use, c+2 loading
+  float* QRb = Wb + 3 * kLgChunk * WS; // [2][32][QRS]: staging of windows c (phase B) and c+1 (phase A)
   __shared__ const float* fptr[64];
   __shared__ double red[kLgThreads / 32];
   __shared__ double meanv[64];
@@ -123,26 +123,11 @@ __global__ void __launch_bounds__(kLgThreads, 1) solve_large_kernel(const SolveA
   const int passes = a.iters + (a.do_stats ? 1 : 0);
   // phase-A tiles of this warp: tile i -> frame block i / 4, row block i % 4
   const int tile0 = warp * TPW;
-  for (int pass = 0; pass < passes; ++pass) {
-    const bool stats_pass = pass == a.iters;
-    const bool want_div = a.div_first ? pass == 0 : stats_pass;
-    float num[MBW][NB][4], den[MBW][NB][4];
-#pragma unroll
-    for (int mb = 0; mb < MBW; ++mb)
-#pragma unroll
-      for (int nb = 0; nb < NB; ++nb)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) num[mb][nb][e] = den[mb][nb][e] = 0.0f;
-    load_w(0, 0);
-    for (int c = 0; c < nch; ++c) {
-      const int c0 = c * kLgChunk, rows = min(kLgChunk, F - c0);
-      const float* Wc = Wb + (c & 1) * kLgChunk * WS;
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-      __syncthreads();  // window c visible; every warp is done with window c-1 and the staging
-      if (c + 1 < nch) load_w(c0 + kLgChunk, (c + 1) & 1);
-
-      // ---------------- phase A: Lam^T = h^T W^T for this warp's tiles, q / r staged
-      {
+      // ---------------- phase A of window c: Lam^T = h^T W^T for this warp's tiles, q / r staged
+  auto phase_a = [&](int c, bool want_div) {
+        const int c0 = c * kLgChunk, rows = min(kLgChunk, F - c0);
+        const float* Wc = Wb + (c % 3) * kLgChunk * WS;
+        float* QR = QRb + (c & 1) * kLgChunk * QRS;
         float acc[TPW][2][4];  // [tile][k-block parity][fragment]
 #pragma unroll
         for (int i = 0; i < TPW; ++i)
@@ -203,8 +188,32 @@ __global__ void __launch_bounds__(kLgThreads, 1) solve_large_kernel(const SolveA
             QR[row * QRS + 64 + n] = valid ? r : 0.0f;
           }
         }
-      }
-      __syncthreads();  // staging complete
+        };
+  for (int pass = 0; pass < passes; ++pass) {
+    const bool stats_pass = pass == a.iters;
+    const bool want_div = a.div_first ? pass == 0 : stats_pass;
+    float num[MBW][NB][4], den[MBW][NB][4];
+#pragma unroll
+    for (int mb = 0; mb < MBW; ++mb)
+#pragma unroll
+      for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) num[mb][nb][e] = den[mb][nb][e] = 0.0f;
+    // windows: c in W buffer c % 3 and staging c & 1; phase A of c+1 and phase B of c
+    // run between the same two barriers
+    load_w(0, 0);
+    if (nch > 1) load_w(kLgChunk, 1);
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncthreads();
+    phase_a(0, want_div);
+    for (int c = 0; c < nch; ++c) {
+      const int c0 = c * kLgChunk, rows = min(kLgChunk, F - c0);
+      const float* Wc = Wb + (c % 3) * kLgChunk * WS;
+      const float* QR = QRb + (c & 1) * kLgChunk * QRS;
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+      __syncthreads();  // staging c complete, window c+1 visible, window c-1 and staging c+1 free
+      if (c + 2 < nch) load_w(c0 + 2 * kLgChunk, (c + 2) % 3);
+      if (c + 1 < nch) phase_a(c + 1, want_div);
 
       if (!stats_pass) {
         // ---------------- phase B: [num|den][k][n] += sum_rows W[row][k] [q|r][row][n]
