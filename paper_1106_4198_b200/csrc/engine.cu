@@ -19,6 +19,7 @@
 #include <random>
 #include <string>
 #include <unordered_set>
+#include <utility>
 #include <vector>
 
 #include "../../include/isnmf_b200.h"
@@ -110,7 +111,32 @@ int ws_for(int KP) { return ((KP / 4) % 2 == 1) ? KP : KP + 4; }
 bool fold_configured = false;
 
 // K2: one cluster of kFoldCluster CTAs per column of W.
-int launch_fold(const FoldArgs& f, cudaStream_t s) {
+// Programmatic dependent launch: the online engine chains K1 -> K2 -> K1 with
+// programmatic stream serialization so each launch overlaps the previous grid's
+// tail (the kernels call griddepcontrol.wait before touching its outputs).
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("ISNMF_PDL");
+    return e ? atoi(e) != 0 : true;
+  }();
+  return on;
+}
+template <class... P, class... A>
+cudaError_t launch_pdl(void (*fn)(P...), int grid, int block, size_t smem, cudaStream_t s, A&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(grid));
+  cfg.blockDim = dim3(unsigned(block));
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, fn, std::forward<A>(args)...);
+}
+
+int launch_fold(const FoldArgs& f, cudaStream_t s, bool pdl = false) {
   const size_t smem = fold_smem_bytes(f.F);
   if (smem + 1024 > size_t(smem_optin()))
     return fail(ISNMF_E_UNSUPPORTED, "F=%d too large for the commit kernel", f.F);
@@ -118,7 +144,10 @@ int launch_fold(const FoldArgs& f, cudaStream_t s) {
     CU(cudaFuncSetAttribute(fold_commit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin() - 1024));
     fold_configured = true;
   }
-  fold_commit_kernel<<<f.K * kFoldCluster, kFoldThreads, smem, s>>>(f);
+  if (pdl && pdl_enabled())
+    CU(launch_pdl(fold_commit_kernel, f.K * kFoldCluster, kFoldThreads, smem, s, f));
+  else
+    fold_commit_kernel<<<f.K * kFoldCluster, kFoldThreads, smem, s>>>(f);
   return 0;
 }
 int fold_parts(int K) { return 2 * K * kFoldCluster; }
@@ -239,9 +268,13 @@ int plan_solve(int64_t F, int64_t K, int64_t frames, SolvePlan* plan, bool force
   return 0;
 }
 
-void launch_solve(const SolvePlan& p, int nblk, const SolveArgs& a, cudaStream_t s) {
-  if (p.large)
+void launch_solve(const SolvePlan& p, int nblk, const SolveArgs& a, cudaStream_t s, bool pdl = false) {
+  if (p.large && pdl && pdl_enabled())
+    launch_pdl(p.large, nblk, p.threads, p.smem, s, a);
+  else if (p.large)
     p.large<<<nblk, p.threads, p.smem, s>>>(a);
+  else if (p.var && pdl && pdl_enabled())
+    launch_pdl(p.var->fn, nblk, kThreads, p.smem, s, a);
   else if (p.var)
     p.var->fn<<<nblk, kThreads, p.smem, s>>>(a);
   else
@@ -504,7 +537,7 @@ int launch_block(isnmf_online* c, const float* dv, int64_t ldv, int nb, const ui
     }
     CU(cudaEventRecord(c->ev_pool[c->ev_used], c->cs));
   }
-  launch_solve(c->plan, nblk, a, c->cs);
+  launch_solve(c->plan, nblk, a, c->cs, !c->prof);
   if (c->prof) {
     CU(cudaEventRecord(c->ev_pool[c->ev_used + 1], c->cs));
     c->ev_used += 2;
@@ -525,7 +558,7 @@ int launch_block(isnmf_online* c, const float* dv, int64_t ldv, int nb, const ui
     }
     CU(cudaEventRecord(c->ev_tail[c->tail_used], c->cs));
   }
-  TRY(launch_fold(r, c->cs));
+  TRY(launch_fold(r, c->cs, !c->prof));
   c->launches += 2;
   if (commit) c->commits_host++;
   if (c->prof) {

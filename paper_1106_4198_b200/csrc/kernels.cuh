@@ -73,6 +73,13 @@ struct DevState {
 #define PROF_MARK(ph)
 #endif
 
+// Programmatic dependent launch (the online engine launches K1 and K2 with
+// programmatic stream serialization): pdl_wait blocks until the preceding grid
+// has completed and its memory is visible (a no-op for a normal launch);
+// pdl_trigger lets the next grid start its launch before this one finishes.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ float rcp_approx(float x) {
   float r;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
@@ -531,6 +538,7 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(const SolveArgs a) {
   using S = SolveShape<TK, TN>;
   using KM = KMap<TK>;
   constexpr int KP = S::KP, NT = S::NT, PBS = S::PBS, WS = S::WS;
+  pdl_wait();
   if (*a.status || (a.halt && *a.halt)) return;
 
   extern __shared__ __align__(16) float smem[];
@@ -761,6 +769,7 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(const SolveArgs a) {
   }
 
   if (a.do_stats) {
+    pdl_trigger();  // K2 may launch onto SMs as CTAs finish
     const bool want_div = !a.div_first || a.iters == 0;
     const int rgs = lane & 7, kgs = lane >> 3;
     for (int c0 = r0; c0 < r1; c0 += kChunk) {
@@ -978,7 +987,7 @@ __device__ __forceinline__ double block_sum_d(double v, double* red) {
 
 __global__ void __cluster_dims__(kFoldCluster, 1, 1) __launch_bounds__(kFoldThreads)
     fold_commit_kernel(const FoldArgs a) {
-  if (a.st->status || *a.halt) return;  // both fixed for the whole launch (see above)
+  pdl_trigger();  // the next K1 may start its launch; it waits for this grid before touching its outputs
   extern __shared__ __align__(16) double fsm[];
   __shared__ double red[kFoldWarps];
   __shared__ double s_cs, s_sc;
@@ -1008,6 +1017,13 @@ __global__ void __cluster_dims__(kFoldCluster, 1, 1) __launch_bounds__(kFoldThre
     }
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
+  // the row state above is written only by the previous K2 (complete before the K1 that
+  // precedes this grid started); the partials and the status come from that K1
+  pdl_wait();
+  if (a.st->status || *a.halt) {  // both fixed for the whole launch (see above)
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    return;
+  }
   // ---- 1. this rank's share of the partial blocks, all rows of column k
   const int NQ = (F + 3) / 4, G = fold_groups(F);
   const int FP = (F + 3) & ~3;

@@ -53,6 +53,7 @@ __global__ void __launch_bounds__(kLgThreads, 1) solve_large_kernel(const SolveA
   using L = LargeShape<MBW, NB>;
   constexpr int KP = L::KP, NT = L::NT, KB = L::KB, FMB = L::FMB, TPW = L::TPW, KPS = L::KPS, WS = L::WS,
                 QRS = L::QRS, HROWS = L::HROWS;
+  pdl_wait();
   if (*a.status || (a.halt && *a.halt)) return;
   extern __shared__ __align__(16) float smem[];
   float* Hs = smem;                   // [HROWS][KPS], zero outside (n < nf, k < K)
@@ -192,6 +193,7 @@ __global__ void __launch_bounds__(kLgThreads, 1) solve_large_kernel(const SolveA
   for (int pass = 0; pass < passes; ++pass) {
     const bool stats_pass = pass == a.iters;
     const bool want_div = a.div_first ? pass == 0 : stats_pass;
+    if (stats_pass) pdl_trigger();  // K2 may launch onto SMs as CTAs finish
     float num[MBW][NB][4], den[MBW][NB][4];
 #pragma unroll
     for (int mb = 0; mb < MBW; ++mb)
