@@ -238,3 +238,17 @@ def test_large_k_tensor_and_generic_kernels_agree():
     s1, s2 = e1.state(), e2.state()
     for k in ("w", "a", "b"):
         assert rel(s1[k], s2[k]) < 1e-5
+
+
+@pytest.mark.parametrize("F,K,beta,iters,N,restart", [
+    (4097, 8, 64, 3, 256, "warm"),   # 8192-point STFT rows: W does not fit shared memory (generic kernel)
+    (65, 300, 64, 2, 128, "fresh"),  # K beyond the tensor-pipe kernel's 256
+])
+def test_extreme_shapes(F, K, beta, iters, N, restart):
+    eng, orc, v = make_pair(F, K, beta, iters, N, restart=restart, rho=0.8)
+    orc.run(v.astype(np.float64))
+    eng.run(v)
+    se, so = eng.state(), orc.state()
+    for k in ("w", "a", "b"):
+        assert rel(se[k], so[k]) < RTOL, (k, rel(se[k], so[k]))
+    assert se["commits"] == so["commits"]
