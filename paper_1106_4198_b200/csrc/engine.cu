@@ -25,6 +25,7 @@
 #include "../../include/isnmf_b200.h"
 #include "kernels.cuh"
 #include "kernels_large.cuh"
+#include "kernels_large_tc.cuh"
 
 using namespace isnmf_dev;
 
@@ -202,6 +203,29 @@ size_t large_smem(int mbw, int nb) {  // = LargeShape<mbw, nb>::smem_bytes()
 static_assert(LargeShape<2, 7>::smem_bytes() == sizeof(float) * (64 * 260 + 3 * 32 * 260 + 2 * 32 * 136),
               "large_smem() mirrors LargeShape::smem_bytes()");
 bool large_configured[2][8] = {};
+// tcgen05 variant (128 < K <= 256), [NB - 1]
+LargeFn g_large_tc[7] = {solve_large_tc_kernel<1>, solve_large_tc_kernel<2>, solve_large_tc_kernel<3>,
+                         solve_large_tc_kernel<4>, solve_large_tc_kernel<5>, solve_large_tc_kernel<6>,
+                         solve_large_tc_kernel<7>};
+size_t large_tc_smem(int nb) {
+  switch (nb) {
+    case 1: return LargeTcShape<1>::smem_bytes();
+    case 2: return LargeTcShape<2>::smem_bytes();
+    case 3: return LargeTcShape<3>::smem_bytes();
+    case 4: return LargeTcShape<4>::smem_bytes();
+    case 5: return LargeTcShape<5>::smem_bytes();
+    case 6: return LargeTcShape<6>::smem_bytes();
+    default: return LargeTcShape<7>::smem_bytes();
+  }
+}
+bool large_tc_configured[7] = {};
+bool tc_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("ISNMF_TC");
+    return e ? atoi(e) != 0 : true;
+  }();
+  return on;
+}
 
 struct SolvePlan {
   LargeFn large = nullptr;  // tensor-pipe kernels (large K, or the resident-dictionary variant)
@@ -231,6 +255,24 @@ int plan_solve(int64_t F, int64_t K, int64_t frames, SolvePlan* plan, bool force
   if (!force_generic && K > 64 && K <= 256) {
     const int nb = int(std::min<int64_t>(8, std::max<int64_t>(1, (per_cta + 7) / 8)));
     const int mbw = K <= 128 ? 1 : 2;
+    if (mbw == 2 && nb <= 7 && tc_enabled()) {  // phase B on tcgen05
+      const size_t smem = large_tc_smem(nb);
+      if (smem + 2048 <= size_t(smem_optin())) {
+        if (!large_tc_configured[nb - 1]) {
+          CU(cudaFuncSetAttribute(g_large_tc[nb - 1], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  smem_optin() - 2048));
+          large_tc_configured[nb - 1] = true;
+        }
+        plan->large = g_large_tc[nb - 1];
+        plan->threads = kTcThreads;
+        plan->var = nullptr;
+        plan->NT = 8 * nb;
+        plan->KP = 256;
+        plan->WS = ws_for(256);
+        plan->smem = smem;
+        return 0;
+      }
+    }
     const size_t smem = large_smem(mbw, nb);
     if (smem + 2048 <= size_t(smem_optin())) {
       if (!large_configured[mbw - 1][nb - 1]) {
