@@ -215,6 +215,7 @@ def test_generic_and_tiled_kernels_agree():
     (129, 80, 96, 4, 300, "fresh"),     # K <= 128: one m-block per warp
     (129, 256, 8192, 2, 8192, "warm"),  # config-4 frames per CTA (56), ragged last window
     (1025, 200, 2048, 3, 2048, "fresh"),  # K padded to 256
+    (129, 200, 9472, 2, 9472, "warm"),    # 64 frames per CTA: the mma.sync kernel (tcgen05 variant holds <= 56)
 ])
 def test_large_k_tensor_kernel(F, K, beta, iters, N, restart):
     """The tensor-pipe kernel (3xTF32 mma.sync, 64 < K <= 256) against the oracle."""
