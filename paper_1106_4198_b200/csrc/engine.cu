@@ -680,8 +680,11 @@ int online_enqueue(isnmf_online* c, const float* frames, int64_t ldv, int64_t n,
   }
   int64_t pos = 0;
   int buf = 0;
+  // chunk sizes ramp up from two mini-batches so the first copy (not overlapped) is short
+  int64_t ramp = 2 * int64_t(c->beta);
   while (pos < n_eff) {
-    const int64_t cf = std::min<int64_t>(c->chunk, n_eff - pos);
+    const int64_t cf = std::min<int64_t>(std::min<int64_t>(c->chunk, ramp), n_eff - pos);
+    ramp *= 2;
     CU(cudaStreamWaitEvent(c->xs, c->ev_free[buf], 0));
     if (ldv == c->F)  // contiguous frames: one linear DMA (2D copies run far below PCIe speed)
       CU(cudaMemcpyAsync(c->vbuf[buf], frames + pos * ldv, size_t(cf) * c->F * sizeof(float),
