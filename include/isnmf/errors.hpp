@@ -93,6 +93,9 @@ inline void check(int rc) {
     case ISNMF_E_NON_FINITE_ENTRY: throw NonFiniteEntry(msg);
     case ISNMF_E_NEGATIVE_ENTRY: throw NegativeEntry(msg);
     case ISNMF_E_IO: throw IoError(msg);
+    case ISNMF_E_UNSUPPORTED_FORMAT: throw UnsupportedFormat(msg);
+    case ISNMF_E_TOO_SHORT: throw TooShort(msg);
+    case ISNMF_E_ALL_SILENT: throw AllSilent(msg);
     default: throw DeviceError(msg);
   }
 }

@@ -1,7 +1,8 @@
 // isnmf-b200 C++ API — umbrella header of the hot-path subset of the
 // reference's proj/include/isnmf/isnmf.hpp plus the §8(f) rows built so far:
-// held-out evaluation, matrix files and checkpoints.  Audio ingest, the
-// experiment grid and report export are not part of this engine.
+// held-out evaluation, matrix files, checkpoints and the spectrogram front end.
+// WAV decoding, the experiment grid and report export are not part of this
+// engine.
 #pragma once
 
 #include "batch.hpp"
@@ -14,3 +15,4 @@
 #include "online.hpp"
 #include "report.hpp"
 #include "rng.hpp"
+#include "spectrogram.hpp"

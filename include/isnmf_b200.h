@@ -44,6 +44,9 @@ typedef enum isnmf_status {
   ISNMF_E_NON_FINITE_ENTRY = 9,   /* NonFiniteEntry    errors.hpp:37-39 */
   ISNMF_E_NEGATIVE_ENTRY = 10,    /* NegativeEntry     errors.hpp:41-43 */
   ISNMF_E_IO = 11,                /* IoError           errors.hpp:25-27 */
+  ISNMF_E_UNSUPPORTED_FORMAT = 12, /* UnsupportedFormat errors.hpp:45-47 */
+  ISNMF_E_TOO_SHORT = 13,         /* TooShort          errors.hpp:49-51 */
+  ISNMF_E_ALL_SILENT = 14,        /* AllSilent         errors.hpp:53-55 */
   ISNMF_E_CUDA = 20,              /* device / driver failure (no reference equivalent) */
   ISNMF_E_INVALID_ARG = 21,       /* bad pointer / size at the C boundary */
   ISNMF_E_UNSUPPORTED = 22        /* shape outside the built kernel family */
@@ -200,6 +203,23 @@ int isnmf_batch_train(const float* v, int64_t ldv, int64_t F, int64_t N, int64_t
  * ------------------------------------------------------------------------- */
 int isnmf_evaluate_heldout(const float* test, int64_t ldt, int64_t F, int64_t N, const double* w, int64_t K,
                            double epsilon, int32_t inner_iters, uint64_t seed, double* out);
+
+/* ---------------------------------------------------------------------------
+ * Spectrogram front end (audio.hpp:121-187).
+ * isnmf_stft_power: sine-windowed one-sided power spectrum of `samples` (fp64,
+ * host), frame i = samples [i*hop, i*hop + window); power is window/2+1 bins x
+ * frames, column-major fp64, frames = (n_samples - window)/hop + 1.  Windows
+ * that are powers of two use an in-shared-memory radix-2 FFT, others a direct
+ * DFT; both in fp64 on the device.  Errors: UnsupportedFormat (window odd or
+ * < 2, hop outside [1, window]), TooShort (signal shorter than one window).
+ * isnmf_discard_silence: indices (ascending) of the frames whose total power is
+ * at least max * 10^(threshold_db/10); spec is bins x frames fp64 (host or
+ * device).  Errors: AllSilent.
+ * ------------------------------------------------------------------------- */
+int isnmf_stft_power(const double* samples, int64_t n_samples, int32_t window, int32_t hop, double* power,
+                     int64_t frames_cap, int64_t* frames);
+int isnmf_discard_silence(const double* spec, int64_t bins, int64_t frames, double threshold_db, int64_t* keep,
+                          int64_t* n_keep);
 
 #ifdef __cplusplus
 }

@@ -21,7 +21,8 @@ HEADER = os.path.join(os.path.dirname(_HERE), "include", "isnmf_b200.h")
 ERRORS = {
     1: "ShapeMismatch", 2: "EmptyDataset", 3: "NegativeInput", 4: "NonPositiveInit", 5: "ZeroColumn",
     6: "InconsistentStats", 7: "NumericalFailure", 8: "DivergedObjective", 9: "NonFiniteEntry",
-    10: "NegativeEntry", 11: "IoError", 20: "CudaError", 21: "InvalidArgument", 22: "Unsupported",
+    10: "NegativeEntry", 11: "IoError", 12: "UnsupportedFormat", 13: "TooShort", 14: "AllSilent",
+    20: "CudaError", 21: "InvalidArgument", 22: "Unsupported",
 }
 RESTART = {"warm": 0, "fresh": 1}
 
@@ -76,6 +77,8 @@ _SIGS = {
     "isnmf_online_profile_end": ([VP, VP, VP, VP, VP, VP], C.c_int),
     "isnmf_batch_train": ([VP, I64, I64, I64, I64, VP, VP, U64, D, D, VP, VP, VP, VP, VP, VP], C.c_int),
     "isnmf_evaluate_heldout": ([VP, I64, I64, I64, VP, I64, D, C.c_int32, U64, VP], C.c_int),
+    "isnmf_stft_power": ([VP, I64, C.c_int32, C.c_int32, VP, I64, VP], C.c_int),
+    "isnmf_discard_silence": ([VP, I64, I64, D, VP, VP], C.c_int),
 }
 
 
@@ -330,3 +333,22 @@ def evaluate_heldout(test32, w, eps=1e-12, inner_iters=100, seed=0x45):
     out = D()
     _check(lib().isnmf_evaluate_heldout(_p(test32), ldt, F, N, _p(w), K, eps, inner_iters, seed, C.byref(out)))
     return out.value
+
+
+def stft_power(samples, window=512, hop=256):
+    """audio.hpp:121-153 on the device: bins x frames fp64 power spectrogram."""
+    x = np.ascontiguousarray(samples, dtype=np.float64)
+    frames = (x.size - window) // hop + 1 if window >= 2 and hop >= 1 and x.size >= window else 0
+    out = np.zeros((window // 2 + 1 if window >= 2 else 1, max(frames, 0)), order="F")
+    got = I64()
+    _check(lib().isnmf_stft_power(_p(x), x.size, window, hop, _p(out), out.shape[1], C.byref(got)))
+    return out
+
+
+def discard_silence(spec, threshold_db=-60.0):
+    """audio.hpp:164-187 on the device: the ascending indices of the retained frames."""
+    spec = np.asfortranarray(spec, dtype=np.float64)
+    keep = np.empty(max(spec.shape[1], 1), dtype=np.int64)
+    n = I64()
+    _check(lib().isnmf_discard_silence(_p(spec), spec.shape[0], spec.shape[1], threshold_db, _p(keep), C.byref(n)))
+    return keep[:n.value].copy()

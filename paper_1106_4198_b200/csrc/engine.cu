@@ -26,6 +26,7 @@
 #include "kernels.cuh"
 #include "kernels_large.cuh"
 #include "kernels_large_tc.cuh"
+#include "stft.cuh"
 
 using namespace isnmf_dev;
 
@@ -1691,6 +1692,106 @@ int isnmf_evaluate_heldout(const float* test, int64_t ldt, int64_t F, int64_t N,
   TRY(wk.state(&h));
   if (h.status) return status_to_code(h.status, "evaluate_heldout", 0);
   *out = h.pending_div / double(N);
+  return 0;
+}
+
+// audio.hpp:121-153 (stft_power) on the device in fp64
+int isnmf_stft_power(const double* samples, int64_t n_samples, int32_t window, int32_t hop, double* power,
+                     int64_t frames_cap, int64_t* frames_out) {
+  if (window < 2 || window % 2 != 0) return fail(ISNMF_E_UNSUPPORTED_FORMAT, "stft_power: window must be even and >= 2");
+  if (hop < 1 || hop > window) return fail(ISNMF_E_UNSUPPORTED_FORMAT, "stft_power: need 1 <= hop <= window");
+  if (n_samples < window) return fail(ISNMF_E_TOO_SHORT, "stft_power: signal shorter than one window");
+  if (!samples || !power || !frames_out) return fail(ISNMF_E_INVALID_ARG, "NULL argument");
+  const int64_t frames = (n_samples - window) / hop + 1;
+  const int bins = window / 2 + 1;
+  *frames_out = frames;
+  if (frames > frames_cap) return fail(ISNMF_E_INVALID_ARG, "stft_power: output holds %lld frames, need %lld",
+                                       (long long)frames_cap, (long long)frames);
+  int logW = 0;
+  while ((1 << logW) < window) ++logW;
+  const bool pow2 = (1 << logW) == window && window <= 4096;
+  if (!pow2 && size_t(window) * sizeof(double) + 4096 > size_t(smem_optin()))
+    return fail(ISNMF_E_UNSUPPORTED, "stft_power: window %d too large", window);
+  std::vector<double> win(static_cast<size_t>(window));
+  std::vector<double2> tw(static_cast<size_t>(window));
+  for (int i = 0; i < window; ++i) {
+    win[size_t(i)] = std::sin(M_PI * (i + 0.5) / window);
+    const double ang = -2.0 * M_PI * double(i) / double(window);
+    tw[size_t(i)] = make_double2(std::cos(ang), std::sin(ang));
+  }
+  cudaStream_t st = nullptr;
+  CU(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  DevBuf bs, bw, bt, bp;
+  double *ds = nullptr, *dw = nullptr, *dp = nullptr;
+  double2* dt = nullptr;
+  int rc = 0;
+  if ((rc = dalloc(&ds, size_t(n_samples))) || (rc = dalloc(&dw, size_t(window))) ||
+      (rc = dalloc(&dt, size_t(window))) || (rc = dalloc(&dp, size_t(frames) * bins))) {
+    dfree(ds);
+    dfree(dw);
+    dfree(dt);
+    dfree(dp);
+    cudaStreamDestroy(st);
+    return rc;
+  }
+  bs.p = ds;
+  bw.p = dw;
+  bt.p = dt;
+  bp.p = dp;
+  CU(cudaMemcpyAsync(ds, samples, size_t(n_samples) * sizeof(double), cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(dw, win.data(), win.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(dt, tw.data(), tw.size() * sizeof(double2), cudaMemcpyHostToDevice, st));
+  for (int64_t f0 = 0; f0 < frames; f0 += 1 << 30) {  // grid.x limit
+    const int nb = int(std::min<int64_t>(frames - f0, int64_t(1) << 30));
+    if (pow2) {
+      const size_t sm = size_t(window) * sizeof(double2);
+      if (sm > 48 * 1024) CU(cudaFuncSetAttribute(stft_fft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+      stft_fft_kernel<<<nb, kStftThreads, sm, st>>>(ds + f0 * hop, window, logW, hop, dw, dt, dp + f0 * bins, bins);
+    } else {
+      const size_t sm = size_t(window) * sizeof(double);
+      if (sm > 48 * 1024) CU(cudaFuncSetAttribute(stft_dft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+      stft_dft_kernel<<<nb, kStftThreads, sm, st>>>(ds + f0 * hop, window, hop, dw, dt, dp + f0 * bins, bins);
+    }
+    CU(cudaGetLastError());
+  }
+  CU(cudaMemcpyAsync(power, dp, size_t(frames) * bins * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  CU(cudaStreamDestroy(st));
+  return 0;
+}
+
+// audio.hpp:164-187 (discard_silence): the indices of the retained frames
+int isnmf_discard_silence(const double* spec, int64_t bins, int64_t frames, double threshold_db, int64_t* keep,
+                          int64_t* n_keep) {
+  if (!spec || !keep || !n_keep) return fail(ISNMF_E_INVALID_ARG, "NULL argument");
+  if (bins < 1 || frames < 1) return fail(ISNMF_E_ALL_SILENT, "discard_silence: every frame is silent");
+  DevBuf bspec, bpow, bkeep, bcnt;
+  const double* dspec = spec;
+  if (!is_device_ptr(spec)) {
+    double* tmp = nullptr;
+    TRY(dalloc(&tmp, size_t(bins) * frames));
+    bspec.p = tmp;
+    CU(cudaMemcpy(tmp, spec, size_t(bins) * frames * sizeof(double), cudaMemcpyHostToDevice));
+    dspec = tmp;
+  }
+  double* dpow = nullptr;
+  int64_t* dkeep = nullptr;
+  int64_t* dcnt = nullptr;
+  TRY(dalloc(&dpow, size_t(frames)));
+  bpow.p = dpow;
+  TRY(dalloc(&dkeep, size_t(frames)));
+  bkeep.p = dkeep;
+  TRY(dalloc(&dcnt, 2));
+  bcnt.p = dcnt;
+  frame_power_kernel<<<int(std::min<int64_t>((frames + 7) / 8, 4096)), 256>>>(dspec, bins, frames, dpow);
+  silence_select_kernel<<<1, kSelThreads>>>(dpow, frames, threshold_db, dkeep, dcnt,
+                                            reinterpret_cast<int*>(dcnt + 1));
+  CU(cudaGetLastError());
+  int64_t hc[2] = {0, 0};
+  CU(cudaMemcpy(hc, dcnt, sizeof(hc), cudaMemcpyDeviceToHost));
+  if (int(hc[1] & 0xffffffff) != 0 || hc[0] == 0) return fail(ISNMF_E_ALL_SILENT, "discard_silence: every frame is silent");
+  CU(cudaMemcpy(keep, dkeep, size_t(hc[0]) * sizeof(int64_t), cudaMemcpyDeviceToHost));
+  *n_keep = hc[0];
   return 0;
 }
 

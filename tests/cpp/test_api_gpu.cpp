@@ -363,3 +363,31 @@ TEST_CASE("evaluate_heldout: frozen W, deterministic, errors (harness.hpp:17-37)
   CHECK_THROWS_AS(evaluate_heldout(w, Matrix::Ones(F + 1, 4), 1e-12), ShapeMismatch);
   CHECK_THROWS_AS(evaluate_heldout(w, Matrix(F, 0), 1e-12), EmptyDataset);
 }
+
+TEST_CASE("stft_power / discard_silence: frame rule, Parseval, order, errors (audio.hpp:121-187)") {
+  std::vector<double> x(4000);
+  for (std::size_t i = 0; i < x.size(); ++i) x[i] = std::sin(0.05 * double(i)) + (i % 7 == 0 ? 0.3 : 0.0);
+  Matrix p = stft_power(x, 512, 256);
+  CHECK(p.rows() == 257 && p.cols() == (4000 - 512) / 256 + 1);
+  // Parseval on frame 0: sum |X_f|^2 over the full spectrum = W * sum (w x)^2
+  double e_time = 0.0;
+  for (int i = 0; i < 512; ++i) {
+    const double w = std::sin(M_PI * (i + 0.5) / 512) * x[std::size_t(i)];
+    e_time += w * w;
+  }
+  double e_freq = p(0, 0) + p(256, 0);
+  for (Index f = 1; f < 256; ++f) e_freq += 2.0 * p(f, 0);
+  CHECK_REL(e_freq, 512.0 * e_time, 1e-10);
+  CHECK_THROWS_AS(stft_power(x, 511, 256), UnsupportedFormat);
+  CHECK_THROWS_AS(stft_power(std::vector<double>(100, 1.0), 512, 256), TooShort);
+  Matrix spec = p;
+  for (Index f = 0; f < spec.rows(); ++f) spec(f, 3) *= 1e-9;  // -90 dB
+  std::vector<FrameMeta> meta(std::size_t(spec.cols()));
+  for (std::size_t i = 0; i < meta.size(); ++i) meta[i] = FrameMeta{7, 100 + i};
+  SpectrogramDataset ds = discard_silence(spec, -60.0, 16000.0, &meta);
+  CHECK(ds.discarded_count == 1 && ds.frames.cols() == spec.cols() - 1 && ds.meta.size() == std::size_t(spec.cols() - 1));
+  CHECK(ds.meta[3].frame_index == 104 && ds.frames(10, 3) == spec(10, 4) && ds.sample_rate == 16000.0);
+  CHECK_THROWS_AS(discard_silence(Matrix::Zero(4, 5)), AllSilent);
+  std::vector<FrameMeta> short_meta(2);
+  CHECK_THROWS_AS(discard_silence(spec, -60.0, 0.0, &short_meta), ShapeMismatch);
+}
