@@ -198,11 +198,30 @@ __global__ void __launch_bounds__(kTcThreads, 1) solve_large_tc_kernel(const Sol
         vv[i][e] = (tile0 + i < 4 * FMB && n < nf && row < rows) ? __ldg(fptr[n] + c0 + row) : 0.0f;
       }
     const float* hrow = Hs + (16 * fmb + g) * KPS + t;
-#pragma unroll 1
-    for (int kb = 0; kb < KB; kb += 2) {
+    // W fragments straight from the swizzled window: for row r = 8 rnb + g and
+    // k = 32 q + 8 u + t, tc_off_a = base(r) + 128 q + ((u ^ r%4) << 3) + t; the
+    // remainder half comes from the lo copy the tensor-core phase B uses
+    const float* wbase[TPW];
+    const float* lbase[TPW];
+    int xo[4];
+    {
+      const int r4 = g & 3;  // row % 4 (8 rnb is a multiple of 4)
 #pragma unroll
-      for (int p = 0; p < 2; ++p) {
-        const float* hp = hrow + 8 * (kb + p);
+      for (int u = 0; u < 4; ++u) xo[u] = ((u ^ r4) << 3) + t;
+#pragma unroll
+      for (int i = 0; i < TPW; ++i) {
+        const int row = 8 * ((tile0 + i) & 3) + g;
+        const int b = (row >> 2) * 8 * 128 + r4 * 32;
+        wbase[i] = Wc + b;
+        lbase[i] = Alo + (c & 1) * AW + b;
+      }
+    }
+#pragma unroll 1
+    for (int q = 0; q < KB / 4; ++q) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int kb = 4 * q + u, p = u & 1;
+        const float* hp = hrow + 8 * kb;
         uint32_t ah[4], al[4];
         split_tf32(hp[0], ah[0], al[0]);
         split_tf32(hp[8 * KPS], ah[1], al[1]);
@@ -211,9 +230,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) solve_large_tc_kernel(const Sol
         uint32_t bh[TPW][2], bl[TPW][2];
 #pragma unroll
         for (int i = 0; i < TPW; ++i) {
-          const int row = 8 * ((tile0 + i) & 3) + g, k = 8 * (kb + p) + t;
-          split_tf32(Wc[tc_off_a(k, row)], bh[i][0], bl[i][0]);
-          split_tf32(Wc[tc_off_a(k + 4, row)], bh[i][1], bl[i][1]);
+          const int o = 128 * q + xo[u];
+          bh[i][0] = __float_as_uint(wbase[i][o]);
+          bh[i][1] = __float_as_uint(wbase[i][o + 4]);
+          bl[i][0] = __float_as_uint(lbase[i][o]);
+          bl[i][1] = __float_as_uint(lbase[i][o + 4]);
         }
 #pragma unroll
         for (int i = 0; i < TPW; ++i) mma_tf32(acc[i][p], al, bh[i][0], bh[i][1]);
