@@ -338,14 +338,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) solve_large_tc_kernel(const Sol
           for (int rm = 0; rm < 2; ++rm) {
             const int r0 = 16 * rm + g, n = 8 * kb + t;
             uint32_t qh[4], ql[4], rh[4], rl[4];
-            split_tf32(Bhi[tc_off_b(n, r0)], qh[0], ql[0]);
-            split_tf32(Bhi[tc_off_b(n, r0 + 8)], qh[1], ql[1]);
-            split_tf32(Bhi[tc_off_b(n + 4, r0)], qh[2], ql[2]);
-            split_tf32(Bhi[tc_off_b(n + 4, r0 + 8)], qh[3], ql[3]);
-            split_tf32(Bhi[tc_off_b(NT + n, r0)], rh[0], rl[0]);
-            split_tf32(Bhi[tc_off_b(NT + n, r0 + 8)], rh[1], rl[1]);
-            split_tf32(Bhi[tc_off_b(NT + n + 4, r0)], rh[2], rl[2]);
-            split_tf32(Bhi[tc_off_b(NT + n + 4, r0 + 8)], rh[3], rl[3]);
+            const int oq[4] = {tc_off_b(n, r0), tc_off_b(n, r0 + 8), tc_off_b(n + 4, r0), tc_off_b(n + 4, r0 + 8)};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {  // hi = raw q / r, lo from the remainder copy phase B uses
+              qh[e] = __float_as_uint(Bhi[oq[e]]);
+              ql[e] = __float_as_uint(Blo[oq[e]]);
+              rh[e] = __float_as_uint(Bhi[oq[e] + NT * 32]);  // tc_off_b(NT + n, r) = tc_off_b(n, r) + 32 NT
+              rl[e] = __float_as_uint(Blo[oq[e] + NT * 32]);
+            }
 #pragma unroll
             for (int j = 0; j < KNW; ++j) {
               mma_tf32(sa[rm][j], ql, hh[j][0], hh[j][1]);
