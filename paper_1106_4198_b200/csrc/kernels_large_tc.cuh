@@ -89,7 +89,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) solve_large_tc_kernel(const Sol
   if (*a.status || (a.halt && *a.halt)) return;
   extern __shared__ __align__(16) float smem_raw[];
   // 1024-byte aligned base for the swizzled operand atoms
-  float* smem = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned base, as an offset from the shared array (keeps the pointers in the shared space)
+  const uint32_t sbase = smem_addr(smem_raw);
+  float* smem = smem_raw + ((((sbase + 1023u) & ~1023u) - sbase) >> 2);
   float* Ahi = smem;               // [2][AW]
   float* Alo = Ahi + 2 * AW;       // [2][AW]
   float* Bhi = Alo + 2 * AW;       // [BW]  raw q / r (the tensor core reads the tf32 part)
