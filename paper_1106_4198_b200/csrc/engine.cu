@@ -26,7 +26,6 @@
 #include "kernels.cuh"
 #include "kernels_large.cuh"
 #include "kernels_large_tc.cuh"
-#include "kernels_res_tc.cuh"
 #include "stft.cuh"
 
 using namespace isnmf_dev;
@@ -239,49 +238,7 @@ struct SolvePlan {
 
 bool generic_configured = false;
 
-// resident-dictionary tcgen05 variant (48 < K <= 64, <= 32 frames per CTA), [NB - 1]
-LargeFn g_res_tc[4] = {solve_res_tc_kernel<1>, solve_res_tc_kernel<2>, solve_res_tc_kernel<3>,
-                       solve_res_tc_kernel<4>};
-bool res_tc_configured[4] = {};
-size_t res_tc_smem(int nb, int F) {
-  switch (nb) {
-    case 1: return ResTcShape<1>::smem_bytes(F);
-    case 2: return ResTcShape<2>::smem_bytes(F);
-    case 3: return ResTcShape<3>::smem_bytes(F);
-    default: return ResTcShape<4>::smem_bytes(F);
-  }
-}
-bool res_enabled() {
-  static const bool on = [] {
-    const char* e = getenv("ISNMF_RES");
-    return e ? atoi(e) != 0 : false;
-  }();
-  return on;
-}
-
 int plan_solve(int64_t F, int64_t K, int64_t frames, SolvePlan* plan, bool force_generic = false) {
-  if (!force_generic && res_enabled() && K > 48 && K <= 64) {
-    const int64_t per_cta = (frames + device_sms() - 1) / device_sms();
-    const int nb = int(std::max<int64_t>(1, (per_cta + 7) / 8));
-    if (nb <= 4) {
-      const size_t smem = res_tc_smem(nb, int(F));
-      if (smem + 2048 <= size_t(smem_optin())) {
-        if (!res_tc_configured[nb - 1]) {
-          CU(cudaFuncSetAttribute(g_res_tc[nb - 1], cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  smem_optin() - 2048));
-          res_tc_configured[nb - 1] = true;
-        }
-        plan->large = g_res_tc[nb - 1];
-        plan->threads = kRsThreads;
-        plan->var = nullptr;
-        plan->NT = 8 * nb;
-        plan->KP = 64;
-        plan->WS = ws_for(64);
-        plan->smem = smem;
-        return 0;
-      }
-    }
-  }
   Variant* v = nullptr;
   int WS = 0;
   size_t sm = 0;

@@ -293,6 +293,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) solve_large_tc_kernel(const Sol
     __syncthreads();
     for (int c = 0; c < nch; ++c) {
       const int c0 = c * kTcRows, rows = min(kTcRows, F - c0);
+#ifdef ISNMF_PHASE_PROF
+      const bool stamp = a.prof && blockIdx.x == 0 && pass == 1 && c < 40;
+#define TC_STAMP(i, who) \
+  if (stamp && tid == (who)) a.prof[c * 8 + (i)] = clock64()
+#else
+#define TC_STAMP(i, who)
+#endif
+      TC_STAMP(0, 32);
       if (!stats_pass) {
         if (tid == 0) {  // phase B of window c on the tensor cores
           asm volatile("tcgen05.fence::after_thread_sync;");
@@ -381,7 +389,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) solve_large_tc_kernel(const Sol
               }
             }
       }
+      TC_STAMP(1, 0);
       if (c + 1 < nch) phase_a(c + 1);  // on the warps while the tensor cores run window c
+      TC_STAMP(2, 32);
       if (!stats_pass) {
         mbar_wait(&mma_bar, mma_phase);  // window c's MMAs are done with A buffer c & 1 and B
         mma_phase ^= 1u;
@@ -389,15 +399,20 @@ __global__ void __launch_bounds__(kTcThreads, 1) solve_large_tc_kernel(const Sol
       } else {
         __syncthreads();  // the statistics are done with B
       }
+      TC_STAMP(3, 32);
       if (c + 1 < nch) phase_a_epilogue(c + 1, want_div);
+      TC_STAMP(4, 32);
       if (c + 2 < nch) {
         store_w(c & 1);
         if (c + 3 < nch) fetch_w(c + 3);
       }
+      TC_STAMP(5, 32);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;");
       __syncthreads();
+      TC_STAMP(6, 32);
     }
+#undef TC_STAMP
     if (!stats_pass) {
       // h update from TMEM: warp (quarter q = warp & 3, column half ch = warp >> 2) reads
       // lanes 32q.. of both k tiles, num at column n, den at column NT + n
