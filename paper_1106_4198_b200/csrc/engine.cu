@@ -26,6 +26,7 @@
 #include "kernels.cuh"
 #include "kernels_large.cuh"
 #include "kernels_large_tc.cuh"
+#include "kernels_mma.cuh"
 #include "stft.cuh"
 
 using namespace isnmf_dev;
@@ -228,6 +229,31 @@ bool tc_enabled() {
   return on;
 }
 
+// K1M: all-tensor-pipe solve for K <= 56, [FG - 1][KB - 1]
+LargeFn g_mma[2][7] = {
+    {solve_mma_kernel<1, 1>, solve_mma_kernel<2, 1>, solve_mma_kernel<3, 1>, solve_mma_kernel<4, 1>,
+     solve_mma_kernel<5, 1>, solve_mma_kernel<6, 1>, solve_mma_kernel<7, 1>},
+    {solve_mma_kernel<1, 2>, solve_mma_kernel<2, 2>, solve_mma_kernel<3, 2>, solve_mma_kernel<4, 2>,
+     solve_mma_kernel<5, 2>, solve_mma_kernel<6, 2>, solve_mma_kernel<7, 2>}};
+size_t mma_smem(int kb, int fg, int F) {
+  const int KP = 8 * kb, NT = 16 * fg, WS = mm_stride(KP), HT = mm_stride(NT);
+  const size_t F16 = size_t((F + 15) & ~15), red = size_t(kMmThreads / 32) * 8 * kb * 32, ht = size_t(KP) * HT;
+  return sizeof(float) * (F16 * WS + size_t(NT) * WS + (red > ht ? red : ht));
+}
+static_assert(MmShape<7, 2>::WS == 56 && MmShape<7, 2>::HT == 40, "K1M strides");
+bool mma_configured[2][7] = {};
+// ISNMF_MMA=0 keeps K <= 56 on the FFMA register-tile kernels; otherwise K1M is
+// used when a CTA gets at least ISNMF_MMA_MIN frames (default 1)
+int mma_min_frames() {
+  static const int v = [] {
+    const char* e = getenv("ISNMF_MMA");
+    if (e && atoi(e) == 0) return 1 << 30;
+    const char* m = getenv("ISNMF_MMA_MIN");
+    return m ? atoi(m) : 1;
+  }();
+  return v;
+}
+
 struct SolvePlan {
   LargeFn large = nullptr;  // tensor-pipe kernels (large K, or the resident-dictionary variant)
   int threads = 0;          // block size of `large`
@@ -242,6 +268,27 @@ int plan_solve(int64_t F, int64_t K, int64_t frames, SolvePlan* plan, bool force
   Variant* v = nullptr;
   int WS = 0;
   size_t sm = 0;
+  if (!force_generic && K >= 1 && K <= 56) {
+    const int64_t per_cta = (frames + device_sms() - 1) / device_sms();
+    const int nt = int(std::min<int64_t>(32, std::max<int64_t>(1, per_cta)));
+    const int kb = int((K + 7) / 8), fg = nt > 16 ? 2 : 1;
+    const size_t smem = mma_smem(kb, fg, int(F));
+    if (nt >= mma_min_frames() && smem + 2048 <= size_t(smem_optin())) {
+      if (!mma_configured[fg - 1][kb - 1]) {
+        CU(cudaFuncSetAttribute(g_mma[fg - 1][kb - 1], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                smem_optin() - 2048));
+        mma_configured[fg - 1][kb - 1] = true;
+      }
+      plan->large = g_mma[fg - 1][kb - 1];
+      plan->threads = kMmThreads;
+      plan->var = nullptr;
+      plan->NT = nt;
+      plan->KP = 8 * kb;
+      plan->WS = mm_stride(8 * kb);
+      plan->smem = smem;
+      return 0;
+    }
+  }
   const int rc = force_generic ? 1 : pick_variant(F, K, frames, &v, &WS, &sm);
   if (rc == 0) {
     plan->var = v;
@@ -311,7 +358,9 @@ int plan_solve(int64_t F, int64_t K, int64_t frames, SolvePlan* plan, bool force
   return 0;
 }
 
-void launch_solve(const SolvePlan& p, int nblk, const SolveArgs& a, cudaStream_t s, bool pdl = false) {
+void launch_solve(const SolvePlan& p, int nblk, const SolveArgs& args, cudaStream_t s, bool pdl = false) {
+  SolveArgs a = args;
+  a.cta_frames = p.NT;
   if (p.large && pdl && pdl_enabled())
     launch_pdl(p.large, nblk, p.threads, p.smem, s, a);
   else if (p.large)
@@ -334,6 +383,16 @@ int dalloc(T** p, size_t n) {
 
 void dfree(void* p) {
   if (p) cudaFree(p);
+}
+
+// Set-up copies/memsets go through the legacy default stream: cudaMemset is
+// asynchronous and a pageable cudaMemcpy H2D may return before its DMA lands,
+// while the engine's streams are non-blocking (no implicit ordering).  Every
+// entry point that stages state that way settles the legacy stream before
+// device work on its own streams may read it.
+int settle() {
+  CU(cudaStreamSynchronize(cudaStreamLegacy));
+  return 0;
 }
 
 bool is_device_ptr(const void* p) {
@@ -797,6 +856,7 @@ int isnmf_online_create(isnmf_online** out, const isnmf_online_config* cfg) {
       cudaMemset(c->pb, 0, FK * sizeof(double)) != cudaSuccess ||
       cudaMemset(c->Hlast, 0, size_t(c->beta) * c->K * sizeof(float)) != cudaSuccess)
     return bail(fail(ISNMF_E_CUDA, "online_create: init failed (%s)", cudaGetErrorString(cudaGetLastError())));
+  if ((rc = settle())) return bail(rc);
   fill_f64<<<64, 256, 0, c->cs>>>(c->P, c->Pcap * c->K, 1.0);
   if (c->restart == ISNMF_RESTART_WARM) {
     fill_f32<<<592, 256, 0, c->cs>>>(c->U, c->nstore * c->K, 1.0f);
@@ -832,7 +892,7 @@ int isnmf_online_set_dictionary(isnmf_online* c, const double* w, const double* 
   }
   if (a) CU(cudaMemcpy(c->A, a, rm.size() * sizeof(double), cudaMemcpyHostToDevice));
   if (b) CU(cudaMemcpy(c->B, b, rm.size() * sizeof(double), cudaMemcpyHostToDevice));
-  return 0;
+  return settle();
 }
 
 int isnmf_online_get_dictionary(isnmf_online* c, double* w, double* a, double* b) {
@@ -860,7 +920,7 @@ int isnmf_online_set_pending(isnmf_online* c, const double* pa, const double* pb
   h.pending_div = pending_div;
   h.pending_count = pending_count;
   CU(cudaMemcpy(c->st, &h, sizeof(h), cudaMemcpyHostToDevice));
-  return 0;
+  return settle();
 }
 
 int isnmf_online_get_pending(isnmf_online* c, double* pa, double* pb, double* pending_div, uint64_t* pending_count) {
@@ -904,7 +964,7 @@ int isnmf_online_set_counters(isnmf_online* c, uint64_t t, uint64_t commits, dou
   c->commits_host = commits;
   c->trace_base = commits;
   c->rho = rho;
-  return 0;
+  return settle();
 }
 
 int isnmf_online_get_counters(isnmf_online* c, uint64_t* t, uint64_t* commits, double* rho, double* last_delta,
@@ -927,6 +987,7 @@ int isnmf_online_set_warm_h(isnmf_online* c, const double* warm_h) {
   for (size_t i = 0; i < u.size(); ++i) u[i] = float(warm_h[i]);
   CU(cudaStreamSynchronize(c->cs));
   CU(cudaMemcpy(c->U, u.data(), u.size() * sizeof(float), cudaMemcpyHostToDevice));
+  TRY(settle());
   fill_u32<<<592, 256, 0, c->cs>>>(c->T, c->nstore, uint32_t(c->commits_host));
   fill_f64<<<1, 256, 0, c->cs>>>(c->P + size_t(c->commits_host) * c->K, c->K, 1.0);
   CU(cudaStreamSynchronize(c->cs));
@@ -1035,6 +1096,7 @@ int isnmf_online_clear_trace(isnmf_online* c) {
   TRY(read_state(c, &h));
   h.trace_base = h.commits;
   CU(cudaMemcpy(c->st, &h, sizeof(h), cudaMemcpyHostToDevice));
+  TRY(settle());
   c->trace_base = h.commits;
   mark_origin<<<1, 1, 0, c->cs>>>(c->st);
   CU(cudaStreamSynchronize(c->cs));
@@ -1265,7 +1327,7 @@ struct SolveWork {
     DevState h{};
     h.last_delta = INFINITY;
     CU(cudaMemcpy(st, &h, sizeof(h), cudaMemcpyHostToDevice));
-    return 0;
+    return settle();
   }
 
   // W from host column-major fp64 (F x K)
@@ -1275,7 +1337,7 @@ struct SolveWork {
     for (int64_t k = 0; k < K; ++k)
       for (int64_t f = 0; f < F; ++f) w32[f * WS + k] = float(w[k * F + f]);
     CU(cudaMemcpy(W32, w32.data(), w32.size() * sizeof(float), cudaMemcpyHostToDevice));
-    return 0;
+    return settle();
   }
 
   // One fused pass over frames [0, n) of V (device, ld ldv): h0 from H (device
@@ -1353,7 +1415,7 @@ int upload_frames(const double* v, int64_t F, int64_t N, float** dv) {
   for (size_t i = 0; i < v32.size(); ++i) v32[i] = float(v[i]);
   TRY(dalloc(dv, v32.size()));
   CU(cudaMemcpy(*dv, v32.data(), v32.size() * sizeof(float), cudaMemcpyHostToDevice));
-  return 0;
+  return settle();
 }
 
 int upload_h(const double* h, int64_t K, int64_t N, float** dh) {
@@ -1361,7 +1423,7 @@ int upload_h(const double* h, int64_t K, int64_t N, float** dh) {
   for (size_t i = 0; i < h32.size(); ++i) h32[i] = float(h[i]);
   TRY(dalloc(dh, std::max<size_t>(1, h32.size())));
   if (!h32.empty()) CU(cudaMemcpy(*dh, h32.data(), h32.size() * sizeof(float), cudaMemcpyHostToDevice));
-  return 0;
+  return settle();
 }
 
 struct DevBuf {
@@ -1652,6 +1714,7 @@ int isnmf_evaluate_heldout(const float* test, int64_t ldt, int64_t F, int64_t N,
     TRY(dalloc(&tmp, size_t(F) * N));
     CU(cudaMemcpy2D(tmp, size_t(F) * sizeof(float), test, size_t(ldt) * sizeof(float), size_t(F) * sizeof(float),
                     size_t(N), cudaMemcpyHostToDevice));
+    TRY(settle());
     bv.p = tmp;
     dv = tmp;
     dld = F;

@@ -131,6 +131,7 @@ struct SolveArgs {
   const int64_t* vsel;  // frame(n) = vsel[n] (nullable)
   int64_t v0;           // frame(n) = v0 + n when vsel == nullptr
   int nframes;
+  int cta_frames;  // frames per CTA of runtime-shaped kernels (K1M); set by launch_solve
   int iters;
   float eps;
   double epsd;

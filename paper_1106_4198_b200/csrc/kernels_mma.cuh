@@ -1,0 +1,491 @@
+// K1M — fused mini-batch solve with every contraction on the tensor pipe, for
+// K <= 8*KB (KB <= 7) and up to 16*FG frames per CTA (config 3: F=513, K=50,
+// 28 frames per CTA).  Same contract as solve_kernel (SolveArgs; solve_h
+// kernels.hpp:62-80, accumulate_sample_stats kernels.hpp:95-108, the
+// divergence online.hpp:303-309).
+//
+// All products are 3xTF32 mma.sync m16n8k8 (lo*hi + hi*lo + hi*hi, fp32
+// accumulate, ~1e-6 relative; hi = the raw fp32 bits, which the tensor core
+// reads as tf32, lo = x minus its tf32 truncation).  mma.sync measured 8.0
+// cycles per m16n8k8 per SM sub-partition with 2 warps x >= 2 chains
+// (tools/probe/mma_probe2.cu), i.e. 1.33x the FP32 FMA peak per useful product
+// and ~10x fewer issued instructions than FFMA register tiles, which is what
+// bounded the FFMA kernel (issue-limited at ~55%).
+//
+// Iterations: warp (fm, rq) owns frames [16fm, 16fm+16) and the rq-th share of
+// the dictionary rows in 8-row blocks; per chunk of up to 4 blocks
+//   phase A  Lam^T[frame][row] = h^T W^T        (M = 16 frames, N = 8 rows, K = k)
+//   q = (v+eps)/Lam^2, r = 1/Lam in registers  (Lam never leaves the registers)
+//   phase B  [num|den]^T[frame][k] += [Q|R]^T W (M = 16 frames, N = 8 k, K = 8 rows)
+// The C fragment of phase A (frame g / g+8, columns 2t, 2t+1) IS the A fragment
+// of phase B once the 8 rows of a block are assigned to the k slots as
+// slot t <-> column 2t, slot t+4 <-> column 2t+1, so q and r are never staged.
+// Rows inside a block are permuted (column n of phase A is row rho(n),
+// rho(g) = g ^ (g >> 2)) so that both phases' dictionary loads are free of
+// bank conflicts with a row stride of 8 or 24 mod 32 words.  The RG warps of a
+// frame group sum their num/den partials in a fixed order through shared memory
+// (bitwise reproducible), then h *= sqrt(num/den).
+//
+// Statistics pass (final h): warps own 16-row blocks and all frames,
+//   Lam[row][frame] = W h                      (M = 16 rows, N = 8 frames, K = k)
+//   [sa|sb][row][k] = [Q|R] h^T               (M = 16 rows, N = 8 k, K = 8 frames)
+// with the same C -> A fragment identity (frame slots 2t, 2t+1), written
+// straight to this CTA's statistics planes (no cross-warp reduction).
+#pragma once
+
+#include "kernels_large.cuh"
+
+namespace isnmf_dev {
+
+constexpr int kMmThreads = 256;  // 8 warps
+
+// smallest stride >= n (a multiple of 8) that is 8 or 24 mod 32 words: the
+// 64-bit fragment loads of a half warp (8-word groups of 4 rows) hit 32 banks
+__host__ __device__ constexpr int mm_stride(int n) {
+  int s = (n + 7) & ~7;
+  while (s % 32 != 8 && s % 32 != 24) s += 8;
+  return s;
+}
+
+template <int KB, int FG>
+struct MmShape {
+  static constexpr int KP = 8 * KB;   // k padded to the MMA k-block
+  static constexpr int NT = 16 * FG;  // frame capacity per CTA
+  static constexpr int RG = 8 / FG;   // row groups per frame group
+  static constexpr int WS = mm_stride(KP);
+  static constexpr int HS = mm_stride(KP);
+  static constexpr int HT = mm_stride(NT);
+  static constexpr int NREG = 8 * KB;  // num + den accumulator floats per lane
+  static size_t smem_bytes(int F) {
+    const size_t F16 = size_t((F + 15) & ~15);
+    const size_t red = size_t(kMmThreads / 32) * NREG * 32;
+    const size_t ht = size_t(KP) * HT;
+    return sizeof(float) * (F16 * WS + size_t(NT) * HS + (red > ht ? red : ht));
+  }
+};
+
+__device__ __forceinline__ int mm_rho(int n) { return n ^ (n >> 2); }
+
+__device__ __forceinline__ float2 lds64(const float* p) { return *reinterpret_cast<const float2*>(p); }
+
+// One chunk of NBK 8-row blocks (rows row0 ...) of an iteration pass: phase A,
+// q/r in registers, phase B into nd[0] (num^T) / nd[1] (den^T).
+template <int KB, int WS, int NBK>
+__device__ __forceinline__ void mm_chunk(const float* Ws, const float* pA, const float* pB, bool okA, bool okB,
+                                         int row0, int F, float eps, const uint32_t (&ah)[KB][4],
+                                         const uint32_t (&al)[KB][4], float (&nd)[2][KB][4], int g, int t,
+                                         bool divon, float& divacc) {
+  const int rg = mm_rho(g), rp = mm_rho(2 * t), rq = mm_rho(2 * t + 1);
+  // V of this lane's cells: c0 (frame g, row rp), c1 (g, rq), c2 (g+8, rp), c3 (g+8, rq)
+  float vv[NBK][4];
+#pragma unroll
+  for (int i = 0; i < NBK; ++i) {
+    const int fp = row0 + 8 * i + rp, fq = row0 + 8 * i + rq;
+    vv[i][0] = (okA && fp < F) ? __ldg(pA + fp) : 0.0f;
+    vv[i][1] = (okA && fq < F) ? __ldg(pA + fq) : 0.0f;
+    vv[i][2] = (okB && fp < F) ? __ldg(pB + fp) : 0.0f;
+    vv[i][3] = (okB && fq < F) ? __ldg(pB + fq) : 0.0f;
+  }
+  // ---- phase A: Lam^T (16 frames x 8 rows per block), NBK independent chains
+  float acc[NBK][4];
+#pragma unroll
+  for (int i = 0; i < NBK; ++i)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[i][c] = 0.0f;
+#pragma unroll
+  for (int kb = 0; kb < KB; ++kb) {
+    uint32_t bh[NBK][2], bl[NBK][2];
+#pragma unroll
+    for (int i = 0; i < NBK; ++i) {
+      const float2 w = lds64(Ws + (row0 + 8 * i + rg) * WS + 8 * kb + 2 * t);
+      split_tf32(w.x, bh[i][0], bl[i][0]);
+      split_tf32(w.y, bh[i][1], bl[i][1]);
+    }
+#pragma unroll
+    for (int i = 0; i < NBK; ++i) mma_tf32(acc[i], al[kb], bh[i][0], bh[i][1]);
+#pragma unroll
+    for (int i = 0; i < NBK; ++i) mma_tf32(acc[i], ah[kb], bl[i][0], bl[i][1]);
+#pragma unroll
+    for (int i = 0; i < NBK; ++i) mma_tf32(acc[i], ah[kb], bh[i][0], bh[i][1]);
+  }
+  // ---- q = (v+eps)/Lam^2, r = 1/Lam (zero outside the valid frames / rows)
+  float q[NBK][4], r[NBK][4];
+#pragma unroll
+  for (int i = 0; i < NBK; ++i)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int f = row0 + 8 * i + ((c & 1) ? rq : rp);
+      const bool valid = ((c < 2) ? okA : okB) && f < F;
+      const float rr = rcp_approx(acc[i][c] + eps);
+      const float ve = vv[i][c] + eps;
+      q[i][c] = valid ? ve * rr * rr : 0.0f;
+      r[i][c] = valid ? rr : 0.0f;
+      if (divon) divacc += valid ? is_term_ratio(ve * rr) : 0.0f;
+    }
+  // ---- phase B: per block, K = its 8 rows (slot t <-> c0/c2, slot t+4 <-> c1/c3)
+#pragma unroll
+  for (int i = 0; i < NBK; ++i) {
+    uint32_t qh[4], ql[4], rh[4], rl[4];
+    split_tf32(q[i][0], qh[0], ql[0]);
+    split_tf32(q[i][2], qh[1], ql[1]);
+    split_tf32(q[i][1], qh[2], ql[2]);
+    split_tf32(q[i][3], qh[3], ql[3]);
+    split_tf32(r[i][0], rh[0], rl[0]);
+    split_tf32(r[i][2], rh[1], rl[1]);
+    split_tf32(r[i][1], rh[2], rl[2]);
+    split_tf32(r[i][3], rh[3], rl[3]);
+    const float* wp = Ws + (row0 + 8 * i + rp) * WS + g;
+    const float* wq = Ws + (row0 + 8 * i + rq) * WS + g;
+    uint32_t bh[KB][2], bl[KB][2];
+#pragma unroll
+    for (int j = 0; j < KB; ++j) {
+      split_tf32(wp[8 * j], bh[j][0], bl[j][0]);
+      split_tf32(wq[8 * j], bh[j][1], bl[j][1]);
+    }
+#pragma unroll
+    for (int j = 0; j < KB; ++j) {
+      mma_tf32(nd[0][j], ql, bh[j][0], bh[j][1]);
+      mma_tf32(nd[1][j], rl, bh[j][0], bh[j][1]);
+    }
+#pragma unroll
+    for (int j = 0; j < KB; ++j) {
+      mma_tf32(nd[0][j], qh, bl[j][0], bl[j][1]);
+      mma_tf32(nd[1][j], rh, bl[j][0], bl[j][1]);
+    }
+#pragma unroll
+    for (int j = 0; j < KB; ++j) {
+      mma_tf32(nd[0][j], qh, bh[j][0], bh[j][1]);
+      mma_tf32(nd[1][j], rh, bh[j][0], bh[j][1]);
+    }
+  }
+}
+
+// One 16-row block of the statistics pass: Lam = W h, q/r (+ divergence), and
+// the block's rows of the statistics planes.
+template <int KB, int FG, int WS, int HS, int HT>
+__device__ __forceinline__ void mm_stats_block(const float* Ws, const float* Hs, const float* Ht,
+                                               const float* const* fptr, int f0, int F, int K, int nf, float eps,
+                                               int g, int t, bool want_div, float& divacc, float* outA,
+                                               float* outB, int FP) {
+  constexpr int NB = 2 * FG;  // frame blocks of 8
+  // c0 (row g, frame 8nb+2t), c1 (g, 2t+1), c2 (g+8, 2t), c3 (g+8, 2t+1)
+  float vv[NB][4];
+#pragma unroll
+  for (int nb = 0; nb < NB; ++nb) {
+    const int na = 8 * nb + 2 * t, nbb = na + 1;
+    const bool ra = f0 + g < F, rb = f0 + g + 8 < F;
+    vv[nb][0] = (na < nf && ra) ? __ldg(fptr[na] + f0 + g) : 0.0f;
+    vv[nb][1] = (nbb < nf && ra) ? __ldg(fptr[nbb] + f0 + g) : 0.0f;
+    vv[nb][2] = (na < nf && rb) ? __ldg(fptr[na] + f0 + g + 8) : 0.0f;
+    vv[nb][3] = (nbb < nf && rb) ? __ldg(fptr[nbb] + f0 + g + 8) : 0.0f;
+  }
+  float acc[NB][4];
+#pragma unroll
+  for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[nb][c] = 0.0f;
+#pragma unroll
+  for (int kb = 0; kb < KB; ++kb) {
+    const float2 x = lds64(Ws + (f0 + g) * WS + 8 * kb + 2 * t);
+    const float2 y = lds64(Ws + (f0 + g + 8) * WS + 8 * kb + 2 * t);
+    uint32_t wh[4], wl[4];
+    split_tf32(x.x, wh[0], wl[0]);
+    split_tf32(y.x, wh[1], wl[1]);
+    split_tf32(x.y, wh[2], wl[2]);
+    split_tf32(y.y, wh[3], wl[3]);
+    uint32_t hh[NB][2], hl[NB][2];
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb) {
+      const float2 h = lds64(Hs + (8 * nb + g) * HS + 8 * kb + 2 * t);
+      split_tf32(h.x, hh[nb][0], hl[nb][0]);
+      split_tf32(h.y, hh[nb][1], hl[nb][1]);
+    }
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb) mma_tf32(acc[nb], wl, hh[nb][0], hh[nb][1]);
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb) mma_tf32(acc[nb], wh, hl[nb][0], hl[nb][1]);
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb) mma_tf32(acc[nb], wh, hh[nb][0], hh[nb][1]);
+  }
+  float q[NB][4], r[NB][4];
+#pragma unroll
+  for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int n = 8 * nb + 2 * t + (c & 1), f = f0 + g + 8 * (c >> 1);
+      const bool valid = n < nf && f < F;
+      const float rr = rcp_approx(acc[nb][c] + eps);
+      const float ve = vv[nb][c] + eps;
+      q[nb][c] = valid ? ve * rr * rr : 0.0f;
+      r[nb][c] = valid ? rr : 0.0f;
+      if (want_div) divacc += valid ? is_term_ratio(ve * rr) : 0.0f;
+    }
+  if (!outA) return;
+  float sa[KB][4], sb[KB][4];
+#pragma unroll
+  for (int j = 0; j < KB; ++j)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) sa[j][c] = sb[j][c] = 0.0f;
+#pragma unroll
+  for (int nb = 0; nb < NB; ++nb) {
+    uint32_t qh[4], ql[4], rh[4], rl[4];
+    split_tf32(q[nb][0], qh[0], ql[0]);
+    split_tf32(q[nb][2], qh[1], ql[1]);
+    split_tf32(q[nb][1], qh[2], ql[2]);
+    split_tf32(q[nb][3], qh[3], ql[3]);
+    split_tf32(r[nb][0], rh[0], rl[0]);
+    split_tf32(r[nb][2], rh[1], rl[1]);
+    split_tf32(r[nb][1], rh[2], rl[2]);
+    split_tf32(r[nb][3], rh[3], rl[3]);
+    uint32_t bh[KB][2], bl[KB][2];
+#pragma unroll
+    for (int j = 0; j < KB; ++j) {
+      const float2 h = lds64(Ht + (8 * j + g) * HT + 8 * nb + 2 * t);
+      split_tf32(h.x, bh[j][0], bl[j][0]);
+      split_tf32(h.y, bh[j][1], bl[j][1]);
+    }
+#pragma unroll
+    for (int j = 0; j < KB; ++j) {
+      mma_tf32(sa[j], ql, bh[j][0], bh[j][1]);
+      mma_tf32(sb[j], rl, bh[j][0], bh[j][1]);
+    }
+#pragma unroll
+    for (int j = 0; j < KB; ++j) {
+      mma_tf32(sa[j], qh, bl[j][0], bl[j][1]);
+      mma_tf32(sb[j], rh, bl[j][0], bl[j][1]);
+    }
+#pragma unroll
+    for (int j = 0; j < KB; ++j) {
+      mma_tf32(sa[j], qh, bh[j][0], bh[j][1]);
+      mma_tf32(sb[j], rh, bh[j][0], bh[j][1]);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < KB; ++j)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int k = 8 * j + 2 * t + (c & 1), f = f0 + g + 8 * (c >> 1);
+      if (k < K && f < F) {
+        outA[size_t(k) * FP + f] = sa[j][c];
+        outB[size_t(k) * FP + f] = sb[j][c];
+      }
+    }
+}
+
+template <int KB, int FG>
+__global__ void __launch_bounds__(kMmThreads, 1) solve_mma_kernel(const SolveArgs a) {
+  using S = MmShape<KB, FG>;
+  constexpr int KP = S::KP, NT = S::NT, RG = S::RG, WS = S::WS, HS = S::HS, HT = S::HT, NREG = S::NREG;
+  pdl_wait();
+  if (*a.status || (a.halt && *a.halt)) return;
+
+  extern __shared__ __align__(16) float smem[];
+  const int F = a.F, K = a.K;
+  const int F16 = (F + 15) & ~15;
+  float* Ws = smem;           // [F16][WS], rows >= F zero
+  float* Hs = Ws + F16 * WS;  // [NT][HS] h (frame-major), zero outside n < nf, k < K
+  float* RED = Hs + NT * HS;  // [8 warps][NREG][32] num/den partials | Ht [KP][HT] (statistics pass)
+  __shared__ const float* fptr[NT];
+  __shared__ double red[kMmThreads / 32];
+  __shared__ double meanv[NT];
+  __shared__ int s_bad;
+  __shared__ __align__(8) unsigned long long wbar;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
+  const int ntc = a.cta_frames;
+  const int n0 = blockIdx.x * ntc;
+  const int nf = min(ntc, a.nframes - n0);
+
+  if (tid == 0) {  // dictionary -> smem by TMA bulk copies, overlapped with the h0 set-up below
+    const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&wbar));
+    const uint32_t bytes = uint32_t(F) * WS * 4u;
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes));
+    const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(Ws));
+    constexpr uint32_t kPiece = 32768;
+    for (uint32_t off = 0; off < bytes; off += kPiece) {
+      const uint32_t n = bytes - off < kPiece ? bytes - off : kPiece;
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       dst + off),
+                   "l"(reinterpret_cast<const char*>(a.W32) + off), "r"(n), "r"(bar)
+                   : "memory");
+    }
+  }
+  for (int i = tid; i < (F16 - F) * WS; i += kMmThreads) Ws[F * WS + i] = 0.0f;  // pad rows
+  if (tid < NT) {
+    const int64_t fr = tid < nf ? (a.vsel ? a.vsel[n0 + tid] : a.v0 + n0 + tid) : 0;
+    fptr[tid] = a.V + fr * a.ldv;
+  }
+  if (tid == 0) s_bad = 0;
+  __syncthreads();
+
+  if (a.h0_mode == 2) {  // mean of each frame in fp64 (fresh_h_init's v.mean())
+    for (int n = warp; n < nf; n += kMmThreads / 32) {
+      double s = 0.0;
+      for (int f = lane; f < F; f += 32) s += double(fptr[n][f]);
+      s = warp_sum_d(s);
+      if (lane == 0) meanv[n] = s / double(F);
+    }
+    __syncthreads();
+  }
+  for (int idx = tid; idx < NT * KP; idx += kMmThreads) {
+    const int n = idx / KP, k = idx - n * KP;
+    float val = 0.0f;
+    if (n < nf && k < K) {
+      if (a.h0_mode == 0) {
+        val = a.H0[size_t(n0 + n) * K + k];
+      } else if (a.h0_mode == 1) {
+        const int64_t col = a.widx ? int64_t(a.widx[n0 + n]) : (a.wbase + n0 + n) % a.wmod;
+        const uint32_t tag = a.T[col];
+        const double ratio = a.P[size_t(a.c_now) * K + k] / a.P[size_t(tag) * K + k];
+        val = float(double(a.U[size_t(col) * K + k]) * ratio);
+      } else {
+        const double mv = meanv[n] > a.epsd ? meanv[n] : a.epsd;
+        val = float(mv / a.kst->kmeanw * a.u01[size_t(n0 + n) * K + k]);
+      }
+      if (a.hscale) val = float(double(val) * a.hscale[k]);
+      if (a.check_h0 && !(val > 0.0f)) s_bad = 1;
+    }
+    Hs[n * HS + k] = val;
+  }
+  {  // wait for the dictionary (phase 0 of wbar)
+    const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&wbar));
+    uint32_t done = 0;
+    while (!done)
+      asm volatile(
+          "{\n\t.reg .pred P;\n\tmbarrier.try_wait.parity.shared::cta.b64 P, [%1], 0;\n\tselp.b32 %0, 1, 0, P;\n\t}\n"
+          : "=r"(done)
+          : "r"(bar)
+          : "memory");
+  }
+  __syncthreads();
+  if (s_bad) {
+    if (tid == 0) atomicOr(a.status, ST_NONPOS_INIT);
+    return;
+  }
+
+  const float eps = a.eps;
+  float divacc = 0.0f;
+  // iteration passes: warp = fm + FG * rq; frame group 1 visits the row groups
+  // in reverse so an uneven block split lands on two different SM sub-partitions
+  const int fm = warp % FG, rq = warp / FG;
+  const int rgi = (FG == 2 && fm == 1) ? RG - 1 - rq : rq;
+  const int NBLK = (F + 7) >> 3;
+  const int blk0 = rgi * NBLK / RG, blk1 = (rgi + 1) * NBLK / RG;
+  const int nA = 16 * fm + g, nB = nA + 8;
+  const bool okA = nA < nf, okB = nB < nf;
+  const float* pA = fptr[nA];
+  const float* pB = fptr[nB];
+
+  for (int pass = 0; pass < a.iters; ++pass) {
+    const bool divon = a.div_first && pass == 0;
+    uint32_t ah[KB][4], al[KB][4];  // h^T A fragments: a0 (g, slot t), a1 (g+8, t), a2 (g, t+4), a3 (g+8, t+4)
+#pragma unroll
+    for (int kb = 0; kb < KB; ++kb) {
+      const float2 x = lds64(Hs + nA * HS + 8 * kb + 2 * t);
+      const float2 y = lds64(Hs + nB * HS + 8 * kb + 2 * t);
+      split_tf32(x.x, ah[kb][0], al[kb][0]);
+      split_tf32(y.x, ah[kb][1], al[kb][1]);
+      split_tf32(x.y, ah[kb][2], al[kb][2]);
+      split_tf32(y.y, ah[kb][3], al[kb][3]);
+    }
+    float nd[2][KB][4];
+#pragma unroll
+    for (int x = 0; x < 2; ++x)
+#pragma unroll
+      for (int j = 0; j < KB; ++j)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) nd[x][j][c] = 0.0f;
+    int cb = blk0;
+#pragma unroll 1
+    for (; cb + 4 <= blk1; cb += 4)
+      mm_chunk<KB, WS, 4>(Ws, pA, pB, okA, okB, 8 * cb, F, eps, ah, al, nd, g, t, divon, divacc);
+    switch (blk1 - cb) {
+      case 3: mm_chunk<KB, WS, 3>(Ws, pA, pB, okA, okB, 8 * cb, F, eps, ah, al, nd, g, t, divon, divacc); break;
+      case 2: mm_chunk<KB, WS, 2>(Ws, pA, pB, okA, okB, 8 * cb, F, eps, ah, al, nd, g, t, divon, divacc); break;
+      case 1: mm_chunk<KB, WS, 1>(Ws, pA, pB, okA, okB, 8 * cb, F, eps, ah, al, nd, g, t, divon, divacc); break;
+      default: break;
+    }
+    {  // partials -> shared memory, lane-contiguous per register (conflict-free)
+      float* rw = RED + warp * NREG * 32 + lane;
+#pragma unroll
+      for (int x = 0; x < 2; ++x)
+#pragma unroll
+        for (int j = 0; j < KB; ++j)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) rw[((x * KB + j) * 4 + c) * 32] = nd[x][j][c];
+    }
+    __syncthreads();
+    // fixed-order sum over the RG row groups, h *= sqrt(num/den) (kernels.hpp:77)
+    constexpr int CELLS = FG * 32 * 4 * KB;
+#pragma unroll
+    for (int m = 0; m < (CELLS + kMmThreads - 1) / kMmThreads; ++m) {
+      const int p = tid + m * kMmThreads;
+      if (p < CELLS) {
+        const int ln = p & 31, rest = p >> 5, jc = rest % (4 * KB), f2 = rest / (4 * KB);
+        const int c = jc & 3, jb = jc >> 2;
+        const int n = 16 * f2 + (ln >> 2) + 8 * (c >> 1), k = 8 * jb + 2 * (ln & 3) + (c & 1);
+        if (n < nf && k < K) {
+          float num = 0.0f, den = 0.0f;
+#pragma unroll
+          for (int r = 0; r < RG; ++r) {
+            const float* src = RED + (f2 + FG * r) * NREG * 32 + ln;
+            num += src[jc * 32];
+            den += src[(4 * KB + jc) * 32];
+          }
+          float& h = Hs[n * HS + k];
+          h = h * sqrtf(num / den);
+        }
+      }
+    }
+    __syncthreads();
+  }
+
+  if (a.do_stats) {
+    pdl_trigger();  // K2 may launch onto SMs as CTAs finish
+    const bool want_div = !a.div_first || a.iters == 0;
+    float* Ht = RED;  // [KP][HT] = h^T (B operand of the statistics contraction)
+    for (int idx = tid; idx < KP * NT; idx += kMmThreads) {
+      const int k = idx / NT, n = idx - k * NT;
+      Ht[k * HT + n] = Hs[n * HS + k];
+    }
+    __syncthreads();
+    const int FP = (F + 3) & ~3;
+    float* outA = a.stats ? a.stats + size_t(blockIdx.x) * 2 * FP * KP : nullptr;
+    float* outB = a.stats ? outA + size_t(FP) * KP : nullptr;
+#pragma unroll 1
+    for (int m = warp; m < F16 / 16; m += kMmThreads / 32)
+      mm_stats_block<KB, FG, WS, HS, HT>(Ws, Hs, Ht, fptr, 16 * m, F, K, nf, eps, g, t, want_div, divacc, outA,
+                                         outB, FP);
+  }
+
+  // divergence partial of this CTA (fixed-order reduction)
+  if (a.divpart) {
+    const double d = warp_sum_d(double(divacc));
+    if (lane == 0) red[warp] = d;
+    __syncthreads();
+    if (tid == 0) {
+      double s = 0.0;
+      for (int w = 0; w < kMmThreads / 32; ++w) s += red[w];
+      a.divpart[blockIdx.x] = s;
+    }
+  }
+
+  // final activations
+  if (a.Hout || a.write_store) {
+    for (int idx = tid; idx < NT * KP; idx += kMmThreads) {
+      const int n = idx / KP, k = idx - n * KP;
+      if (n >= nf || k >= K) continue;
+      const float h = Hs[n * HS + k];
+      if (a.Hout) a.Hout[size_t(n0 + n) * K + k] = h;
+      if (a.write_store) {
+        const int64_t col = a.widx ? int64_t(a.widx[n0 + n]) : (a.wbase + n0 + n) % a.wmod;
+        a.U[size_t(col) * K + k] = h;
+        if (k == 0) a.T[col] = a.c_now;
+      }
+    }
+  }
+}
+
+}  // namespace isnmf_dev
