@@ -66,6 +66,22 @@ struct MmShape {
 
 __device__ __forceinline__ int mm_rho(int n) { return n ^ (n >> 2); }
 
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// barrier of one frame group's warps (named barrier 1 + fm; all warps when FG = 1)
+template <int FG>
+__device__ __forceinline__ void group_sync_t(int fm) {
+  if constexpr (FG == 1) {
+    __syncthreads();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + fm), "r"(kMmThreads / FG) : "memory");
+  }
+}
+
 __device__ __forceinline__ float2 lds64(const float* p) { return *reinterpret_cast<const float2*>(p); }
 
 // One chunk of NBK 8-row blocks (rows row0 ...) of an iteration pass: phase A,
@@ -367,9 +383,13 @@ __global__ void __launch_bounds__(kMmThreads, 1) solve_mma_kernel(const SolveArg
 
   const float eps = a.eps;
   float divacc = 0.0f;
-  // iteration passes: warp = fm + FG * rq; frame group 1 visits the row groups
-  // in reverse so an uneven block split lands on two different SM sub-partitions
-  const int fm = warp % FG, rq = warp / FG;
+  auto group_sync = [](int fm) { group_sync_t<FG>(fm); };
+  // iteration passes: warp = RG * fm + rq, so every SM sub-partition (warp % 4)
+  // hosts one warp of each frame group; the groups synchronise on their own
+  // named barrier, so one group's reduction/update overlaps the other's MMAs.
+  // Frame group 1 visits the row groups in reverse: an uneven block split puts
+  // its extra block on a different sub-partition than group 0's.
+  const int fm = warp / RG, rq = warp % RG;
   const int rgi = (FG == 2 && fm == 1) ? RG - 1 - rq : rq;
   const int NBLK = (F + 7) >> 3;
   const int blk0 = rgi * NBLK / RG, blk1 = (rgi + 1) * NBLK / RG;
@@ -416,31 +436,33 @@ __global__ void __launch_bounds__(kMmThreads, 1) solve_mma_kernel(const SolveArg
 #pragma unroll
           for (int c = 0; c < 4; ++c) rw[((x * KB + j) * 4 + c) * 32] = nd[x][j][c];
     }
-    __syncthreads();
+    group_sync(fm);
     // fixed-order sum over the RG row groups, h *= sqrt(num/den) (kernels.hpp:77)
-    constexpr int CELLS = FG * 32 * 4 * KB;
+    constexpr int CELLS = 32 * 4 * KB;  // per frame group, over its RG * 32 threads
+    const int gt = tid - fm * RG * 32;
 #pragma unroll
-    for (int m = 0; m < (CELLS + kMmThreads - 1) / kMmThreads; ++m) {
-      const int p = tid + m * kMmThreads;
+    for (int m = 0; m < (CELLS + RG * 32 - 1) / (RG * 32); ++m) {
+      const int p = gt + m * RG * 32;
       if (p < CELLS) {
-        const int ln = p & 31, rest = p >> 5, jc = rest % (4 * KB), f2 = rest / (4 * KB);
+        const int ln = p & 31, jc = p >> 5;
         const int c = jc & 3, jb = jc >> 2;
-        const int n = 16 * f2 + (ln >> 2) + 8 * (c >> 1), k = 8 * jb + 2 * (ln & 3) + (c & 1);
+        const int n = 16 * fm + (ln >> 2) + 8 * (c >> 1), k = 8 * jb + 2 * (ln & 3) + (c & 1);
         if (n < nf && k < K) {
           float num = 0.0f, den = 0.0f;
 #pragma unroll
           for (int r = 0; r < RG; ++r) {
-            const float* src = RED + (f2 + FG * r) * NREG * 32 + ln;
+            const float* src = RED + (fm * RG + r) * NREG * 32 + ln;
             num += src[jc * 32];
             den += src[(4 * KB + jc) * 32];
           }
           float& h = Hs[n * HS + k];
-          h = h * sqrtf(num / den);
+          h = h * sqrt_approx(num * rcp_approx(den));
         }
       }
     }
-    __syncthreads();
+    group_sync(fm);
   }
+  __syncthreads();
 
   if (a.do_stats) {
     pdl_trigger();  // K2 may launch onto SMs as CTAs finish
