@@ -229,21 +229,28 @@ bool tc_enabled() {
   return on;
 }
 
-// K1M: all-tensor-pipe solve for K <= 56, [FG - 1][KB - 1]
-LargeFn g_mma[2][7] = {
-    {solve_mma_kernel<1, 1>, solve_mma_kernel<2, 1>, solve_mma_kernel<3, 1>, solve_mma_kernel<4, 1>,
-     solve_mma_kernel<5, 1>, solve_mma_kernel<6, 1>, solve_mma_kernel<7, 1>},
-    {solve_mma_kernel<1, 2>, solve_mma_kernel<2, 2>, solve_mma_kernel<3, 2>, solve_mma_kernel<4, 2>,
-     solve_mma_kernel<5, 2>, solve_mma_kernel<6, 2>, solve_mma_kernel<7, 2>}};
-size_t mma_smem(int kb, int fg, int F) {
+// K1M: all-tensor-pipe solve for K <= 56, [NW == 12][FG - 1][KB - 1]
+#define MM(kb, fg, nw) solve_mma_kernel<kb, fg, nw>
+#define MMROW(fg, nw) {MM(1, fg, nw), MM(2, fg, nw), MM(3, fg, nw), MM(4, fg, nw), MM(5, fg, nw), MM(6, fg, nw), MM(7, fg, nw)}
+LargeFn g_mma[2][2][7] = {{MMROW(1, 8), MMROW(2, 8)}, {MMROW(1, 12), MMROW(2, 12)}};
+#undef MMROW
+#undef MM
+size_t mma_smem(int kb, int fg, int nw, int F) {
   const int KP = 8 * kb, NT = 16 * fg, WS = mm_stride(KP), HT = mm_stride(NT);
-  const size_t F16 = size_t((F + 15) & ~15), red = size_t(kMmThreads / 32) * 8 * kb * 32, ht = size_t(KP) * HT;
-  return sizeof(float) * (F16 * WS + size_t(NT) * WS + (red > ht ? red : ht));
+  const size_t F16 = size_t((F + 15) & ~15), red = size_t(nw) * 8 * kb * 32, ht = size_t(KP) * HT;
+  return sizeof(float) * (F16 * WS + size_t(NT) * WS + size_t(fg) * kb * 256 + (red > ht ? red : ht));
 }
-static_assert(MmShape<7, 2>::WS == 56 && MmShape<7, 2>::HT == 40, "K1M strides");
-bool mma_configured[2][7] = {};
+static_assert(MmShape<7, 2, 12>::WS == 56 && MmShape<7, 2, 12>::HT == 40, "K1M strides");
+bool mma_configured[2][2][7] = {};
 // ISNMF_MMA=0 keeps K <= 56 on the FFMA register-tile kernels; otherwise K1M is
 // used when a CTA gets at least ISNMF_MMA_MIN frames (default 1)
+int mma_warps() {  // ISNMF_MMA_WARPS = 8 or 12 (default 12 when the CTA fits)
+  static const int v = [] {
+    const char* e = getenv("ISNMF_MMA_WARPS");
+    return (e && atoi(e) == 8) ? 8 : 12;
+  }();
+  return v;
+}
 int mma_min_frames() {
   static const int v = [] {
     const char* e = getenv("ISNMF_MMA");
@@ -272,15 +279,18 @@ int plan_solve(int64_t F, int64_t K, int64_t frames, SolvePlan* plan, bool force
     const int64_t per_cta = (frames + device_sms() - 1) / device_sms();
     const int nt = int(std::min<int64_t>(32, std::max<int64_t>(1, per_cta)));
     const int kb = int((K + 7) / 8), fg = nt > 16 ? 2 : 1;
-    const size_t smem = mma_smem(kb, fg, int(F));
+    int nw = mma_warps();
+    if (nw == 12 && mma_smem(kb, fg, 12, int(F)) + 2048 > size_t(smem_optin())) nw = 8;
+    const size_t smem = mma_smem(kb, fg, nw, int(F));
+    const int wi = nw == 12 ? 1 : 0;
     if (nt >= mma_min_frames() && smem + 2048 <= size_t(smem_optin())) {
-      if (!mma_configured[fg - 1][kb - 1]) {
-        CU(cudaFuncSetAttribute(g_mma[fg - 1][kb - 1], cudaFuncAttributeMaxDynamicSharedMemorySize,
+      if (!mma_configured[wi][fg - 1][kb - 1]) {
+        CU(cudaFuncSetAttribute(g_mma[wi][fg - 1][kb - 1], cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 smem_optin() - 2048));
-        mma_configured[fg - 1][kb - 1] = true;
+        mma_configured[wi][fg - 1][kb - 1] = true;
       }
-      plan->large = g_mma[fg - 1][kb - 1];
-      plan->threads = kMmThreads;
+      plan->large = g_mma[wi][fg - 1][kb - 1];
+      plan->threads = 32 * nw;
       plan->var = nullptr;
       plan->NT = nt;
       plan->KP = 8 * kb;

@@ -37,7 +37,7 @@
 
 namespace isnmf_dev {
 
-constexpr int kMmThreads = 256;  // 8 warps
+constexpr int kMmWarpsMax = 12;
 
 // smallest stride >= n (a multiple of 8) that is 8 or 24 mod 32 words: the
 // 64-bit fragment loads of a half warp (8-word groups of 4 rows) hit 32 banks
@@ -47,20 +47,21 @@ __host__ __device__ constexpr int mm_stride(int n) {
   return s;
 }
 
-template <int KB, int FG>
+template <int KB, int FG, int NW>
 struct MmShape {
   static constexpr int KP = 8 * KB;   // k padded to the MMA k-block
   static constexpr int NT = 16 * FG;  // frame capacity per CTA
-  static constexpr int RG = 8 / FG;   // row groups per frame group
+  static constexpr int RG = NW / FG;  // row groups per frame group
   static constexpr int WS = mm_stride(KP);
   static constexpr int HS = mm_stride(KP);
   static constexpr int HT = mm_stride(NT);
-  static constexpr int NREG = 8 * KB;  // num + den accumulator floats per lane
+  static constexpr int NREG = 8 * KB;         // num + den accumulator floats per lane
+  static constexpr int HF = FG * KB * 32 * 8;  // h^T A fragments, [fm][kb][lane][hi 4 | lo 4]
   static size_t smem_bytes(int F) {
     const size_t F16 = size_t((F + 15) & ~15);
-    const size_t red = size_t(kMmThreads / 32) * NREG * 32;
+    const size_t red = size_t(NW) * NREG * 32;
     const size_t ht = size_t(KP) * HT;
-    return sizeof(float) * (F16 * WS + size_t(NT) * HS + (red > ht ? red : ht));
+    return sizeof(float) * (F16 * WS + size_t(NT) * HS + HF + (red > ht ? red : ht));
   }
 };
 
@@ -73,24 +74,38 @@ __device__ __forceinline__ float sqrt_approx(float x) {
 }
 
 // barrier of one frame group's warps (named barrier 1 + fm; all warps when FG = 1)
-template <int FG>
+template <int FG, int NW>
 __device__ __forceinline__ void group_sync_t(int fm) {
   if constexpr (FG == 1) {
     __syncthreads();
   } else {
-    asm volatile("bar.sync %0, %1;" ::"r"(1 + fm), "r"(kMmThreads / FG) : "memory");
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + fm), "r"(32 * NW / FG) : "memory");
   }
+}
+
+// position of h[n][k] in the fragment copy: lane (g, t) of block (fm, kb) holds
+// a0 = (g, 2t), a1 = (g+8, 2t), a2 = (g, 2t+1), a3 = (g+8, 2t+1); lo at +4
+template <int KB>
+__device__ __forceinline__ int hf_index(int n, int k) {
+  const int fm = n >> 4, nn = n & 15, kb = k >> 3, kk = k & 7;
+  const int ln = 4 * (nn & 7) + (kk >> 1), ai = (nn >> 3) + 2 * (kk & 1);
+  return ((fm * KB + kb) * 32 + ln) * 8 + ai;
+}
+__device__ __forceinline__ void put_hf(float* p, float h) {
+  uint32_t hi, lo;
+  split_tf32(h, hi, lo);
+  p[0] = __uint_as_float(hi);
+  p[4] = __uint_as_float(lo);
 }
 
 __device__ __forceinline__ float2 lds64(const float* p) { return *reinterpret_cast<const float2*>(p); }
 
 // One chunk of NBK 8-row blocks (rows row0 ...) of an iteration pass: phase A,
 // q/r in registers, phase B into nd[0] (num^T) / nd[1] (den^T).
-template <int KB, int WS, int NBK>
+template <int KB, int WS, int NBK, bool DIV>
 __device__ __forceinline__ void mm_chunk(const float* Ws, const float* pA, const float* pB, bool okA, bool okB,
-                                         int row0, int F, float eps, const uint32_t (&ah)[KB][4],
-                                         const uint32_t (&al)[KB][4], float (&nd)[2][KB][4], int g, int t,
-                                         bool divon, float& divacc) {
+                                         int row0, int F, float eps, const float* hf, float (&nd)[2][KB][4],
+                                         int g, int t, float& divacc) {
   const int rg = mm_rho(g), rp = mm_rho(2 * t), rq = mm_rho(2 * t + 1);
   // V of this lane's cells: c0 (frame g, row rp), c1 (g, rq), c2 (g+8, rp), c3 (g+8, rq)
   float vv[NBK][4];
@@ -110,6 +125,19 @@ __device__ __forceinline__ void mm_chunk(const float* Ws, const float* pA, const
     for (int c = 0; c < 4; ++c) acc[i][c] = 0.0f;
 #pragma unroll
   for (int kb = 0; kb < KB; ++kb) {
+    uint32_t ah[4], al[4];  // h^T A fragments (pre-split): a0 (g, slot t), a1 (g+8, t), a2 (g, t+4), a3 (g+8, t+4)
+    {
+      const float4 x = *reinterpret_cast<const float4*>(hf + kb * 256);
+      const float4 y = *reinterpret_cast<const float4*>(hf + kb * 256 + 4);
+      ah[0] = __float_as_uint(x.x);
+      ah[1] = __float_as_uint(x.y);
+      ah[2] = __float_as_uint(x.z);
+      ah[3] = __float_as_uint(x.w);
+      al[0] = __float_as_uint(y.x);
+      al[1] = __float_as_uint(y.y);
+      al[2] = __float_as_uint(y.z);
+      al[3] = __float_as_uint(y.w);
+    }
     uint32_t bh[NBK][2], bl[NBK][2];
 #pragma unroll
     for (int i = 0; i < NBK; ++i) {
@@ -118,11 +146,11 @@ __device__ __forceinline__ void mm_chunk(const float* Ws, const float* pA, const
       split_tf32(w.y, bh[i][1], bl[i][1]);
     }
 #pragma unroll
-    for (int i = 0; i < NBK; ++i) mma_tf32(acc[i], al[kb], bh[i][0], bh[i][1]);
+    for (int i = 0; i < NBK; ++i) mma_tf32(acc[i], al, bh[i][0], bh[i][1]);
 #pragma unroll
-    for (int i = 0; i < NBK; ++i) mma_tf32(acc[i], ah[kb], bl[i][0], bl[i][1]);
+    for (int i = 0; i < NBK; ++i) mma_tf32(acc[i], ah, bl[i][0], bl[i][1]);
 #pragma unroll
-    for (int i = 0; i < NBK; ++i) mma_tf32(acc[i], ah[kb], bh[i][0], bh[i][1]);
+    for (int i = 0; i < NBK; ++i) mma_tf32(acc[i], ah, bh[i][0], bh[i][1]);
   }
   // ---- q = (v+eps)/Lam^2, r = 1/Lam (zero outside the valid frames / rows)
   float q[NBK][4], r[NBK][4];
@@ -136,7 +164,7 @@ __device__ __forceinline__ void mm_chunk(const float* Ws, const float* pA, const
       const float ve = vv[i][c] + eps;
       q[i][c] = valid ? ve * rr * rr : 0.0f;
       r[i][c] = valid ? rr : 0.0f;
-      if (divon) divacc += valid ? is_term_ratio(ve * rr) : 0.0f;
+      if constexpr (DIV) divacc += valid ? is_term_ratio(ve * rr) : 0.0f;
     }
   // ---- phase B: per block, K = its 8 rows (slot t <-> c0/c2, slot t+4 <-> c1/c3)
 #pragma unroll
@@ -276,22 +304,33 @@ __device__ __forceinline__ void mm_stats_block(const float* Ws, const float* Hs,
       mma_tf32(sb[j], rh, bh[j][0], bh[j][1]);
     }
   }
+  // planes are [KP][FP]: rows k >= K hold zeros (h = 0 there), so only f is guarded
+  float* pa = outA + size_t(2 * t) * FP + f0 + g;
+  float* pb = outB + size_t(2 * t) * FP + f0 + g;
+  const bool ok0 = f0 + g < F, ok1 = f0 + g + 8 < F;
 #pragma unroll
-  for (int j = 0; j < KB; ++j)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int k = 8 * j + 2 * t + (c & 1), f = f0 + g + 8 * (c >> 1);
-      if (k < K && f < F) {
-        outA[size_t(k) * FP + f] = sa[j][c];
-        outB[size_t(k) * FP + f] = sb[j][c];
-      }
+  for (int j = 0; j < KB; ++j) {
+    const size_t o = size_t(8 * j) * FP;
+    if (ok0) {
+      pa[o] = sa[j][0];
+      pa[o + FP] = sa[j][1];
+      pb[o] = sb[j][0];
+      pb[o + FP] = sb[j][1];
     }
+    if (ok1) {
+      pa[o + 8] = sa[j][2];
+      pa[o + FP + 8] = sa[j][3];
+      pb[o + 8] = sb[j][2];
+      pb[o + FP + 8] = sb[j][3];
+    }
+  }
 }
 
-template <int KB, int FG>
-__global__ void __launch_bounds__(kMmThreads, 1) solve_mma_kernel(const SolveArgs a) {
-  using S = MmShape<KB, FG>;
+template <int KB, int FG, int NW>
+__global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a) {
+  using S = MmShape<KB, FG, NW>;
   constexpr int KP = S::KP, NT = S::NT, RG = S::RG, WS = S::WS, HS = S::HS, HT = S::HT, NREG = S::NREG;
+  constexpr int kMmThreads = 32 * NW;
   pdl_wait();
   if (*a.status || (a.halt && *a.halt)) return;
 
@@ -300,7 +339,8 @@ __global__ void __launch_bounds__(kMmThreads, 1) solve_mma_kernel(const SolveArg
   const int F16 = (F + 15) & ~15;
   float* Ws = smem;           // [F16][WS], rows >= F zero
   float* Hs = Ws + F16 * WS;  // [NT][HS] h (frame-major), zero outside n < nf, k < K
-  float* RED = Hs + NT * HS;  // [8 warps][NREG][32] num/den partials | Ht [KP][HT] (statistics pass)
+  float* Hf = Hs + NT * HS;   // [FG][KB][32][8] pre-split h^T A fragments of the iteration passes
+  float* RED = Hf + S::HF;    // [NW][NREG][32] num/den partials | Ht [KP][HT] (statistics pass)
   __shared__ const float* fptr[NT];
   __shared__ double red[kMmThreads / 32];
   __shared__ double meanv[NT];
@@ -364,6 +404,7 @@ __global__ void __launch_bounds__(kMmThreads, 1) solve_mma_kernel(const SolveArg
       if (a.check_h0 && !(val > 0.0f)) s_bad = 1;
     }
     Hs[n * HS + k] = val;
+    put_hf(Hf + hf_index<KB>(n, k), val);
   }
   {  // wait for the dictionary (phase 0 of wbar)
     const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&wbar));
@@ -383,7 +424,7 @@ __global__ void __launch_bounds__(kMmThreads, 1) solve_mma_kernel(const SolveArg
 
   const float eps = a.eps;
   float divacc = 0.0f;
-  auto group_sync = [](int fm) { group_sync_t<FG>(fm); };
+  auto group_sync = [](int fm) { group_sync_t<FG, NW>(fm); };
   // iteration passes: warp = RG * fm + rq, so every SM sub-partition (warp % 4)
   // hosts one warp of each frame group; the groups synchronise on their own
   // named barrier, so one group's reduction/update overlaps the other's MMAs.
@@ -399,17 +440,7 @@ __global__ void __launch_bounds__(kMmThreads, 1) solve_mma_kernel(const SolveArg
   const float* pB = fptr[nB];
 
   for (int pass = 0; pass < a.iters; ++pass) {
-    const bool divon = a.div_first && pass == 0;
-    uint32_t ah[KB][4], al[KB][4];  // h^T A fragments: a0 (g, slot t), a1 (g+8, t), a2 (g, t+4), a3 (g+8, t+4)
-#pragma unroll
-    for (int kb = 0; kb < KB; ++kb) {
-      const float2 x = lds64(Hs + nA * HS + 8 * kb + 2 * t);
-      const float2 y = lds64(Hs + nB * HS + 8 * kb + 2 * t);
-      split_tf32(x.x, ah[kb][0], al[kb][0]);
-      split_tf32(y.x, ah[kb][1], al[kb][1]);
-      split_tf32(x.y, ah[kb][2], al[kb][2]);
-      split_tf32(y.y, ah[kb][3], al[kb][3]);
-    }
+    const float* hf = Hf + fm * KB * 256 + lane * 8;
     float nd[2][KB][4];
 #pragma unroll
     for (int x = 0; x < 2; ++x)
@@ -418,13 +449,17 @@ __global__ void __launch_bounds__(kMmThreads, 1) solve_mma_kernel(const SolveArg
 #pragma unroll
         for (int c = 0; c < 4; ++c) nd[x][j][c] = 0.0f;
     int cb = blk0;
+    if (a.div_first && pass == 0) {  // batch: the objective of the incoming (W, H) from this pass
+#pragma unroll 1
+      for (; cb < blk1; ++cb) mm_chunk<KB, WS, 1, true>(Ws, pA, pB, okA, okB, 8 * cb, F, eps, hf, nd, g, t, divacc);
+    }
 #pragma unroll 1
     for (; cb + 4 <= blk1; cb += 4)
-      mm_chunk<KB, WS, 4>(Ws, pA, pB, okA, okB, 8 * cb, F, eps, ah, al, nd, g, t, divon, divacc);
+      mm_chunk<KB, WS, 4, false>(Ws, pA, pB, okA, okB, 8 * cb, F, eps, hf, nd, g, t, divacc);
     switch (blk1 - cb) {
-      case 3: mm_chunk<KB, WS, 3>(Ws, pA, pB, okA, okB, 8 * cb, F, eps, ah, al, nd, g, t, divon, divacc); break;
-      case 2: mm_chunk<KB, WS, 2>(Ws, pA, pB, okA, okB, 8 * cb, F, eps, ah, al, nd, g, t, divon, divacc); break;
-      case 1: mm_chunk<KB, WS, 1>(Ws, pA, pB, okA, okB, 8 * cb, F, eps, ah, al, nd, g, t, divon, divacc); break;
+      case 3: mm_chunk<KB, WS, 3, false>(Ws, pA, pB, okA, okB, 8 * cb, F, eps, hf, nd, g, t, divacc); break;
+      case 2: mm_chunk<KB, WS, 2, false>(Ws, pA, pB, okA, okB, 8 * cb, F, eps, hf, nd, g, t, divacc); break;
+      case 1: mm_chunk<KB, WS, 1, false>(Ws, pA, pB, okA, okB, 8 * cb, F, eps, hf, nd, g, t, divacc); break;
       default: break;
     }
     {  // partials -> shared memory, lane-contiguous per register (conflict-free)
@@ -457,6 +492,7 @@ __global__ void __launch_bounds__(kMmThreads, 1) solve_mma_kernel(const SolveArg
           }
           float& h = Hs[n * HS + k];
           h = h * sqrt_approx(num * rcp_approx(den));
+          put_hf(Hf + ((fm * KB + jb) * 32 + ln) * 8 + (c >> 1) + 2 * (c & 1), h);
         }
       }
     }
