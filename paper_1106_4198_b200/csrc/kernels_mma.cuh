@@ -83,19 +83,21 @@ __device__ __forceinline__ void group_sync_t(int fm) {
   }
 }
 
-// position of h[n][k] in the fragment copy: lane (g, t) of block (fm, kb) holds
-// a0 = (g, 2t), a1 = (g+8, 2t), a2 = (g, 2t+1), a3 = (g+8, 2t+1); lo at +4
+// position of h[n][k] in the fragment copy [fm][kb][hi | lo][lane][4]: lane (g, t)
+// of block (fm, kb) holds a0 = (g, 2t), a1 = (g+8, 2t), a2 = (g, 2t+1),
+// a3 = (g+8, 2t+1); the lo copy is 128 floats on (16-byte lane records,
+// conflict-free LDS.128)
 template <int KB>
 __device__ __forceinline__ int hf_index(int n, int k) {
   const int fm = n >> 4, nn = n & 15, kb = k >> 3, kk = k & 7;
   const int ln = 4 * (nn & 7) + (kk >> 1), ai = (nn >> 3) + 2 * (kk & 1);
-  return ((fm * KB + kb) * 32 + ln) * 8 + ai;
+  return (fm * KB + kb) * 256 + ln * 4 + ai;
 }
 __device__ __forceinline__ void put_hf(float* p, float h) {
   uint32_t hi, lo;
   split_tf32(h, hi, lo);
   p[0] = __uint_as_float(hi);
-  p[4] = __uint_as_float(lo);
+  p[128] = __uint_as_float(lo);
 }
 
 __device__ __forceinline__ float2 lds64(const float* p) { return *reinterpret_cast<const float2*>(p); }
@@ -128,7 +130,7 @@ __device__ __forceinline__ void mm_chunk(const float* Ws, const float* pA, const
     uint32_t ah[4], al[4];  // h^T A fragments (pre-split): a0 (g, slot t), a1 (g+8, t), a2 (g, t+4), a3 (g+8, t+4)
     {
       const float4 x = *reinterpret_cast<const float4*>(hf + kb * 256);
-      const float4 y = *reinterpret_cast<const float4*>(hf + kb * 256 + 4);
+      const float4 y = *reinterpret_cast<const float4*>(hf + kb * 256 + 128);
       ah[0] = __float_as_uint(x.x);
       ah[1] = __float_as_uint(x.y);
       ah[2] = __float_as_uint(x.z);
@@ -206,14 +208,10 @@ __device__ __forceinline__ void mm_chunk(const float* Ws, const float* pA, const
 
 // One 16-row block of the statistics pass: Lam = W h, q/r (+ divergence), and
 // the block's rows of the statistics planes.
-template <int KB, int FG, int WS, int HS, int HT>
-__device__ __forceinline__ void mm_stats_block(const float* Ws, const float* Hs, const float* Ht,
-                                               const float* const* fptr, int f0, int F, int K, int nf, float eps,
-                                               int g, int t, bool want_div, float& divacc, float* outA,
-                                               float* outB, int FP) {
-  constexpr int NB = 2 * FG;  // frame blocks of 8
-  // c0 (row g, frame 8nb+2t), c1 (g, 2t+1), c2 (g+8, 2t), c3 (g+8, 2t+1)
-  float vv[NB][4];
+// V of a statistics block's cells: c0 (row g, frame 8nb+2t), c1 (g, 2t+1), c2 (g+8, 2t), c3 (g+8, 2t+1)
+template <int NB>
+__device__ __forceinline__ void mm_stats_v(float (&vv)[NB][4], const float* const* fptr, int f0, int F, int nf,
+                                           int g, int t) {
 #pragma unroll
   for (int nb = 0; nb < NB; ++nb) {
     const int na = 8 * nb + 2 * t, nbb = na + 1;
@@ -223,6 +221,14 @@ __device__ __forceinline__ void mm_stats_block(const float* Ws, const float* Hs,
     vv[nb][2] = (na < nf && rb) ? __ldg(fptr[na] + f0 + g + 8) : 0.0f;
     vv[nb][3] = (nbb < nf && rb) ? __ldg(fptr[nbb] + f0 + g + 8) : 0.0f;
   }
+}
+
+template <int KB, int FG, int WS, int HS, int HT>
+__device__ __forceinline__ void mm_stats_block(const float* Ws, const float* Hs, const float* Ht,
+                                               const float* const* fptr, int f0, int F, int nf, float eps, int g,
+                                               int t, bool want_div, float& divacc, float* outA, float* outB, int FP,
+                                               float (&vv)[2 * FG][4], int f0n) {
+  constexpr int NB = 2 * FG;  // frame blocks of 8
   float acc[NB][4];
 #pragma unroll
   for (int nb = 0; nb < NB; ++nb)
@@ -257,13 +263,15 @@ __device__ __forceinline__ void mm_stats_block(const float* Ws, const float* Hs,
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       const int n = 8 * nb + 2 * t + (c & 1), f = f0 + g + 8 * (c >> 1);
+      const float vc = vv[nb][c];
       const bool valid = n < nf && f < F;
       const float rr = rcp_approx(acc[nb][c] + eps);
-      const float ve = vv[nb][c] + eps;
+      const float ve = vc + eps;
       q[nb][c] = valid ? ve * rr * rr : 0.0f;
       r[nb][c] = valid ? rr : 0.0f;
       if (want_div) divacc += valid ? is_term_ratio(ve * rr) : 0.0f;
     }
+  if (f0n >= 0) mm_stats_v<NB>(vv, fptr, f0n, F, nf, g, t);  // the next block's V, behind the MMAs below
   if (!outA) return;
   float sa[KB][4], sb[KB][4];
 #pragma unroll
@@ -440,7 +448,7 @@ __global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a
   const float* pB = fptr[nB];
 
   for (int pass = 0; pass < a.iters; ++pass) {
-    const float* hf = Hf + fm * KB * 256 + lane * 8;
+    const float* hf = Hf + fm * KB * 256 + lane * 4;
     float nd[2][KB][4];
 #pragma unroll
     for (int x = 0; x < 2; ++x)
@@ -492,7 +500,7 @@ __global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a
           }
           float& h = Hs[n * HS + k];
           h = h * sqrt_approx(num * rcp_approx(den));
-          put_hf(Hf + ((fm * KB + jb) * 32 + ln) * 8 + (c >> 1) + 2 * (c & 1), h);
+          put_hf(Hf + (fm * KB + jb) * 256 + ln * 4 + (c >> 1) + 2 * (c & 1), h);
         }
       }
     }
@@ -512,10 +520,14 @@ __global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a
     const int FP = (F + 3) & ~3;
     float* outA = a.stats ? a.stats + size_t(blockIdx.x) * 2 * FP * KP : nullptr;
     float* outB = a.stats ? outA + size_t(FP) * KP : nullptr;
+    float vv[2 * FG][4];
+    if (warp < F16 / 16) mm_stats_v<2 * FG>(vv, fptr, 16 * warp, F, nf, g, t);
 #pragma unroll 1
-    for (int m = warp; m < F16 / 16; m += kMmThreads / 32)
-      mm_stats_block<KB, FG, WS, HS, HT>(Ws, Hs, Ht, fptr, 16 * m, F, K, nf, eps, g, t, want_div, divacc, outA,
-                                         outB, FP);
+    for (int m = warp; m < F16 / 16; m += kMmThreads / 32) {
+      const int mn = m + kMmThreads / 32;
+      mm_stats_block<KB, FG, WS, HS, HT>(Ws, Hs, Ht, fptr, 16 * m, F, nf, eps, g, t, want_div, divacc, outA, outB,
+                                         FP, vv, mn < F16 / 16 ? 16 * mn : -1);
+    }
   }
 
   // divergence partial of this CTA (fixed-order reduction)
