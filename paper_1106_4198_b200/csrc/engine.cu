@@ -238,9 +238,10 @@ LargeFn g_mma[2][2][7] = {{MMROW(1, 8), MMROW(2, 8)}, {MMROW(1, 12), MMROW(2, 12
 size_t mma_smem(int kb, int fg, int nw, int F) {
   const int KP = 8 * kb, NT = 16 * fg, WS = mm_stride(KP), HT = mm_stride(NT);
   const size_t F16 = size_t((F + 15) & ~15), red = size_t(nw) * 8 * kb * 32, ht = size_t(KP) * HT;
-  return sizeof(float) * (F16 * WS + size_t(NT) * WS + size_t(fg) * kb * 256 + (red > ht ? red : ht));
+  return sizeof(float) * (F16 * WS + size_t(fg) * kb * 256 + (red > ht ? red : ht));
 }
 static_assert(MmShape<7, 2, 12>::WS == 56 && MmShape<7, 2, 12>::HT == 40, "K1M strides");
+static_assert(MmShape<7, 2, 12>::HF == 2 * 7 * 256, "K1M fragment copy = mma_smem()");
 bool mma_configured[2][2][7] = {};
 // ISNMF_MMA=0 keeps K <= 56 on the FFMA register-tile kernels; otherwise K1M is
 // used when a CTA gets at least ISNMF_MMA_MIN frames (default 1)

@@ -53,7 +53,6 @@ struct MmShape {
   static constexpr int NT = 16 * FG;  // frame capacity per CTA
   static constexpr int RG = NW / FG;  // row groups per frame group
   static constexpr int WS = mm_stride(KP);
-  static constexpr int HS = mm_stride(KP);
   static constexpr int HT = mm_stride(NT);
   static constexpr int NREG = 8 * KB;         // num + den accumulator floats per lane
   static constexpr int HF = FG * KB * 32 * 8;  // h^T A fragments, [fm][kb][lane][hi 4 | lo 4]
@@ -61,11 +60,37 @@ struct MmShape {
     const size_t F16 = size_t((F + 15) & ~15);
     const size_t red = size_t(NW) * NREG * 32;
     const size_t ht = size_t(KP) * HT;
-    return sizeof(float) * (F16 * WS + size_t(NT) * HS + HF + (red > ht ? red : ht));
+    return sizeof(float) * (F16 * WS + HF + (red > ht ? red : ht));
   }
 };
 
 __device__ __forceinline__ int mm_rho(int n) { return n ^ (n >> 2); }
+
+// Timeline stamps of CTA 0 (ISNMF_PHASE_PROF builds): prof[warp * 64 + event] = clock64()
+#ifdef ISNMF_PHASE_PROF
+#define MM_STAMP(ev)                                                                     \
+  do {                                                                                   \
+    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && a.prof && (ev) < 64)                \
+      a.prof[(threadIdx.x >> 5) * 64 + (ev)] = clock64();                                \
+  } while (0)
+#define MM_STAMP_P(prof, ev)                                                             \
+  do {                                                                                   \
+    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && (prof) && (ev) < 64)                \
+      (prof)[(threadIdx.x >> 5) * 64 + (ev)] = clock64();                                \
+  } while (0)
+#else
+#define MM_STAMP(ev)
+#define MM_STAMP_P(prof, ev)
+#endif
+
+// is_term (kernels.hpp:15-18) of ratio = (v+eps)/Lam as u - log(ratio) with the
+// fast log: absolute error ~1e-7 per cell (the series of is_term_ratio only
+// buys relative accuracy on terms that are themselves ~1e-7); used for the
+// online objective of the statistics pass
+__device__ __forceinline__ float is_term_fast(float ratio) {
+  const float t = (ratio - 1.0f) - __logf(ratio);
+  return t > 0.0f ? t : 0.0f;
+}
 
 __device__ __forceinline__ float sqrt_approx(float x) {
   float r;
@@ -168,7 +193,19 @@ __device__ __forceinline__ void mm_chunk(const float* Ws, const float* pA, const
       r[i][c] = valid ? rr : 0.0f;
       if constexpr (DIV) divacc += valid ? is_term_ratio(ve * rr) : 0.0f;
     }
-  // ---- phase B: per block, K = its 8 rows (slot t <-> c0/c2, slot t+4 <-> c1/c3)
+  // ---- phase B: per block, K = its 8 rows (slot t <-> c0/c2, slot t+4 <-> c1/c3);
+  // the dictionary values of block i+1 are loaded while block i's MMAs issue
+  float wv[KB][2];
+  auto load_wb = [&](int i) {
+    const float* wp = Ws + (row0 + 8 * i + rp) * WS + g;
+    const float* wq = Ws + (row0 + 8 * i + rq) * WS + g;
+#pragma unroll
+    for (int j = 0; j < KB; ++j) {
+      wv[j][0] = wp[8 * j];
+      wv[j][1] = wq[8 * j];
+    }
+  };
+  load_wb(0);
 #pragma unroll
   for (int i = 0; i < NBK; ++i) {
     uint32_t qh[4], ql[4], rh[4], rl[4];
@@ -180,14 +217,13 @@ __device__ __forceinline__ void mm_chunk(const float* Ws, const float* pA, const
     split_tf32(r[i][2], rh[1], rl[1]);
     split_tf32(r[i][1], rh[2], rl[2]);
     split_tf32(r[i][3], rh[3], rl[3]);
-    const float* wp = Ws + (row0 + 8 * i + rp) * WS + g;
-    const float* wq = Ws + (row0 + 8 * i + rq) * WS + g;
     uint32_t bh[KB][2], bl[KB][2];
 #pragma unroll
     for (int j = 0; j < KB; ++j) {
-      split_tf32(wp[8 * j], bh[j][0], bl[j][0]);
-      split_tf32(wq[8 * j], bh[j][1], bl[j][1]);
+      split_tf32(wv[j][0], bh[j][0], bl[j][0]);
+      split_tf32(wv[j][1], bh[j][1], bl[j][1]);
     }
+    if (i + 1 < NBK) load_wb(i + 1);
 #pragma unroll
     for (int j = 0; j < KB; ++j) {
       mma_tf32(nd[0][j], ql, bh[j][0], bh[j][1]);
@@ -223,12 +259,13 @@ __device__ __forceinline__ void mm_stats_v(float (&vv)[NB][4], const float* cons
   }
 }
 
-template <int KB, int FG, int WS, int HS, int HT>
-__device__ __forceinline__ void mm_stats_block(const float* Ws, const float* Hs, const float* Ht,
+template <int KB, int FG, int WS, int HT>
+__device__ __forceinline__ void mm_stats_block(const float* Ws, const float* Hf, const float* Ht,
                                                const float* const* fptr, int f0, int F, int nf, float eps, int g,
                                                int t, bool want_div, float& divacc, float* outA, float* outB, int FP,
-                                               float (&vv)[2 * FG][4], int f0n) {
+                                               float (&vv)[2 * FG][4], int f0n, long long* prof, int ev) {
   constexpr int NB = 2 * FG;  // frame blocks of 8
+  MM_STAMP_P(prof, ev);
   float acc[NB][4];
 #pragma unroll
   for (int nb = 0; nb < NB; ++nb)
@@ -243,12 +280,22 @@ __device__ __forceinline__ void mm_stats_block(const float* Ws, const float* Hs,
     split_tf32(y.x, wh[1], wl[1]);
     split_tf32(x.y, wh[2], wl[2]);
     split_tf32(y.y, wh[3], wl[3]);
+    // h (k 8kb+2t, 2t+1) of frames 8nb+g from the pre-split fragment records:
+    // frame block 2fm is (a0, a2) of record (fm, kb, lane), block 2fm+1 is (a1, a3)
     uint32_t hh[NB][2], hl[NB][2];
 #pragma unroll
-    for (int nb = 0; nb < NB; ++nb) {
-      const float2 h = lds64(Hs + (8 * nb + g) * HS + 8 * kb + 2 * t);
-      split_tf32(h.x, hh[nb][0], hl[nb][0]);
-      split_tf32(h.y, hh[nb][1], hl[nb][1]);
+    for (int fm = 0; fm < FG; ++fm) {
+      const float* rec = Hf + (fm * KB + kb) * 256 + (4 * g + t) * 4;
+      const float4 x = *reinterpret_cast<const float4*>(rec);
+      const float4 y = *reinterpret_cast<const float4*>(rec + 128);
+      hh[2 * fm][0] = __float_as_uint(x.x);
+      hh[2 * fm][1] = __float_as_uint(x.z);
+      hh[2 * fm + 1][0] = __float_as_uint(x.y);
+      hh[2 * fm + 1][1] = __float_as_uint(x.w);
+      hl[2 * fm][0] = __float_as_uint(y.x);
+      hl[2 * fm][1] = __float_as_uint(y.z);
+      hl[2 * fm + 1][0] = __float_as_uint(y.y);
+      hl[2 * fm + 1][1] = __float_as_uint(y.w);
     }
 #pragma unroll
     for (int nb = 0; nb < NB; ++nb) mma_tf32(acc[nb], wl, hh[nb][0], hh[nb][1]);
@@ -257,6 +304,7 @@ __device__ __forceinline__ void mm_stats_block(const float* Ws, const float* Hs,
 #pragma unroll
     for (int nb = 0; nb < NB; ++nb) mma_tf32(acc[nb], wh, hh[nb][0], hh[nb][1]);
   }
+  MM_STAMP_P(prof, ev + 1);
   float q[NB][4], r[NB][4];
 #pragma unroll
   for (int nb = 0; nb < NB; ++nb)
@@ -269,9 +317,10 @@ __device__ __forceinline__ void mm_stats_block(const float* Ws, const float* Hs,
       const float ve = vc + eps;
       q[nb][c] = valid ? ve * rr * rr : 0.0f;
       r[nb][c] = valid ? rr : 0.0f;
-      if (want_div) divacc += valid ? is_term_ratio(ve * rr) : 0.0f;
+      if (want_div) divacc += valid ? is_term_fast(ve * rr) : 0.0f;
     }
   if (f0n >= 0) mm_stats_v<NB>(vv, fptr, f0n, F, nf, g, t);  // the next block's V, behind the MMAs below
+  MM_STAMP_P(prof, ev + 2);
   if (!outA) return;
   float sa[KB][4], sb[KB][4];
 #pragma unroll
@@ -312,6 +361,7 @@ __device__ __forceinline__ void mm_stats_block(const float* Ws, const float* Hs,
       mma_tf32(sb[j], rh, bh[j][0], bh[j][1]);
     }
   }
+  MM_STAMP_P(prof, ev + 3);
   // planes are [KP][FP]: rows k >= K hold zeros (h = 0 there), so only f is guarded
   float* pa = outA + size_t(2 * t) * FP + f0 + g;
   float* pb = outB + size_t(2 * t) * FP + f0 + g;
@@ -337,7 +387,7 @@ __device__ __forceinline__ void mm_stats_block(const float* Ws, const float* Hs,
 template <int KB, int FG, int NW>
 __global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a) {
   using S = MmShape<KB, FG, NW>;
-  constexpr int KP = S::KP, NT = S::NT, RG = S::RG, WS = S::WS, HS = S::HS, HT = S::HT, NREG = S::NREG;
+  constexpr int KP = S::KP, NT = S::NT, RG = S::RG, WS = S::WS, HT = S::HT, NREG = S::NREG;
   constexpr int kMmThreads = 32 * NW;
   pdl_wait();
   if (*a.status || (a.halt && *a.halt)) return;
@@ -346,8 +396,9 @@ __global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a
   const int F = a.F, K = a.K;
   const int F16 = (F + 15) & ~15;
   float* Ws = smem;           // [F16][WS], rows >= F zero
-  float* Hs = Ws + F16 * WS;  // [NT][HS] h (frame-major), zero outside n < nf, k < K
-  float* Hf = Hs + NT * HS;   // [FG][KB][32][8] pre-split h^T A fragments of the iteration passes
+  // h lives only as its pre-split fragment copy (hi = the raw fp32 value), zero
+  // outside n < nf, k < K: [FG][KB][hi | lo][32 lanes][4]
+  float* Hf = Ws + F16 * WS;
   float* RED = Hf + S::HF;    // [NW][NREG][32] num/den partials | Ht [KP][HT] (statistics pass)
   __shared__ const float* fptr[NT];
   __shared__ double red[kMmThreads / 32];
@@ -411,7 +462,6 @@ __global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a
       if (a.hscale) val = float(double(val) * a.hscale[k]);
       if (a.check_h0 && !(val > 0.0f)) s_bad = 1;
     }
-    Hs[n * HS + k] = val;
     put_hf(Hf + hf_index<KB>(n, k), val);
   }
   {  // wait for the dictionary (phase 0 of wbar)
@@ -430,6 +480,7 @@ __global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a
     return;
   }
 
+  MM_STAMP(0);
   const float eps = a.eps;
   float divacc = 0.0f;
   auto group_sync = [](int fm) { group_sync_t<FG, NW>(fm); };
@@ -470,51 +521,75 @@ __global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a
       case 1: mm_chunk<KB, WS, 1, false>(Ws, pA, pB, okA, okB, 8 * cb, F, eps, hf, nd, g, t, divacc); break;
       default: break;
     }
-    {  // partials -> shared memory, lane-contiguous per register (conflict-free)
-      float* rw = RED + warp * NREG * 32 + lane;
+    MM_STAMP(1 + 4 * pass);
+    {  // partials -> shared memory as [warp][num|den][jb][lane][4] (16-byte lane records)
+      float* rw = RED + warp * NREG * 32 + lane * 4;
 #pragma unroll
       for (int x = 0; x < 2; ++x)
 #pragma unroll
         for (int j = 0; j < KB; ++j)
-#pragma unroll
-          for (int c = 0; c < 4; ++c) rw[((x * KB + j) * 4 + c) * 32] = nd[x][j][c];
+          *reinterpret_cast<float4*>(rw + (x * KB + j) * 128) = make_float4(nd[x][j][0], nd[x][j][1], nd[x][j][2],
+                                                                            nd[x][j][3]);
     }
     group_sync(fm);
-    // fixed-order sum over the RG row groups, h *= sqrt(num/den) (kernels.hpp:77)
-    constexpr int CELLS = 32 * 4 * KB;  // per frame group, over its RG * 32 threads
+    MM_STAMP(2 + 4 * pass);
+    // fixed-order sum over the RG row groups, h *= sqrt(num/den) (kernels.hpp:77); one
+    // thread per (k block, lane) record = 4 cells, h read from / written to the fragment copy
+    constexpr int RECS = 32 * KB;  // per frame group, over its RG * 32 threads
     const int gt = tid - fm * RG * 32;
 #pragma unroll
-    for (int m = 0; m < (CELLS + RG * 32 - 1) / (RG * 32); ++m) {
+    for (int m = 0; m < (RECS + RG * 32 - 1) / (RG * 32); ++m) {
       const int p = gt + m * RG * 32;
-      if (p < CELLS) {
-        const int ln = p & 31, jc = p >> 5;
-        const int c = jc & 3, jb = jc >> 2;
-        const int n = 16 * fm + (ln >> 2) + 8 * (c >> 1), k = 8 * jb + 2 * (ln & 3) + (c & 1);
-        if (n < nf && k < K) {
-          float num = 0.0f, den = 0.0f;
+      if (p < RECS) {
+        const int ln = p & 31, jb = p >> 5;
+        float4 num = make_float4(0.0f, 0.0f, 0.0f, 0.0f), den = num;
 #pragma unroll
-          for (int r = 0; r < RG; ++r) {
-            const float* src = RED + (fm * RG + r) * NREG * 32 + ln;
-            num += src[jc * 32];
-            den += src[(4 * KB + jc) * 32];
-          }
-          float& h = Hs[n * HS + k];
-          h = h * sqrt_approx(num * rcp_approx(den));
-          put_hf(Hf + (fm * KB + jb) * 256 + ln * 4 + (c >> 1) + 2 * (c & 1), h);
+        for (int r = 0; r < RG; ++r) {
+          const float* src = RED + (fm * RG + r) * NREG * 32 + jb * 128 + ln * 4;
+          const float4 x = *reinterpret_cast<const float4*>(src);
+          const float4 y = *reinterpret_cast<const float4*>(src + KB * 128);
+          num.x += x.x;
+          num.y += x.y;
+          num.z += x.z;
+          num.w += x.w;
+          den.x += y.x;
+          den.y += y.y;
+          den.z += y.z;
+          den.w += y.w;
         }
+        // C order (c0 (g, 2t), c1 (g, 2t+1), c2 (g+8, 2t), c3 (g+8, 2t+1)) -> record order a0 a2 a1 a3
+        float* rec = Hf + (fm * KB + jb) * 256 + ln * 4;
+        float4 h = *reinterpret_cast<const float4*>(rec);
+        const int n0c = 16 * fm + (ln >> 2), k0c = 8 * jb + 2 * (ln & 3);
+        const bool v0 = n0c < nf, v1 = n0c + 8 < nf, e0 = k0c < K, e1 = k0c + 1 < K;
+        h.x = (v0 && e0) ? h.x * sqrt_approx(num.x * rcp_approx(den.x)) : h.x;
+        h.z = (v0 && e1) ? h.z * sqrt_approx(num.y * rcp_approx(den.y)) : h.z;
+        h.y = (v1 && e0) ? h.y * sqrt_approx(num.z * rcp_approx(den.z)) : h.y;
+        h.w = (v1 && e1) ? h.w * sqrt_approx(num.w * rcp_approx(den.w)) : h.w;
+        uint32_t hi, lo[4];
+        split_tf32(h.x, hi, lo[0]);
+        split_tf32(h.y, hi, lo[1]);
+        split_tf32(h.z, hi, lo[2]);
+        split_tf32(h.w, hi, lo[3]);
+        *reinterpret_cast<float4*>(rec) = h;
+        *reinterpret_cast<float4*>(rec + 128) = make_float4(__uint_as_float(lo[0]), __uint_as_float(lo[1]),
+                                                            __uint_as_float(lo[2]), __uint_as_float(lo[3]));
       }
     }
+    MM_STAMP(3 + 4 * pass);
     group_sync(fm);
+    MM_STAMP(4 + 4 * pass);
   }
   __syncthreads();
+  MM_STAMP(60);
+  float* Ht = RED;  // [KP][HT] = h^T, B operand of the statistics contraction (RED is free now)
 
   if (a.do_stats) {
     pdl_trigger();  // K2 may launch onto SMs as CTAs finish
     const bool want_div = !a.div_first || a.iters == 0;
-    float* Ht = RED;  // [KP][HT] = h^T (B operand of the statistics contraction)
     for (int idx = tid; idx < KP * NT; idx += kMmThreads) {
       const int k = idx / NT, n = idx - k * NT;
-      Ht[k * HT + n] = Hs[n * HS + k];
+      Ht[k * HT + n] = Hf[hf_index<KB>(n, k)];
     }
     __syncthreads();
     const int FP = (F + 3) & ~3;
@@ -525,11 +600,13 @@ __global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a
 #pragma unroll 1
     for (int m = warp; m < F16 / 16; m += kMmThreads / 32) {
       const int mn = m + kMmThreads / 32;
-      mm_stats_block<KB, FG, WS, HS, HT>(Ws, Hs, Ht, fptr, 16 * m, F, nf, eps, g, t, want_div, divacc, outA, outB,
-                                         FP, vv, mn < F16 / 16 ? 16 * mn : -1);
+      mm_stats_block<KB, FG, WS, HT>(Ws, Hf, Ht, fptr, 16 * m, F, nf, eps, g, t, want_div, divacc, outA, outB,
+                                         FP, vv, mn < F16 / 16 ? 16 * mn : -1, a.prof,
+                                         44 + 4 * ((m - warp) / (kMmThreads / 32)));
     }
   }
 
+  MM_STAMP(61);
   // divergence partial of this CTA (fixed-order reduction)
   if (a.divpart) {
     const double d = warp_sum_d(double(divacc));
@@ -547,7 +624,7 @@ __global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a
     for (int idx = tid; idx < NT * KP; idx += kMmThreads) {
       const int n = idx / KP, k = idx - n * KP;
       if (n >= nf || k >= K) continue;
-      const float h = Hs[n * HS + k];
+      const float h = Hf[hf_index<KB>(n, k)];
       if (a.Hout) a.Hout[size_t(n0 + n) * K + k] = h;
       if (a.write_store) {
         const int64_t col = a.widx ? int64_t(a.widx[n0 + n]) : (a.wbase + n0 + n) % a.wmod;
