@@ -149,6 +149,11 @@ def dist_done(world):
         dist.destroy_process_group()
 
 
+# useful-product ceiling of 3xTF32 on the legacy mma.sync pipe: m16n8k8 TF32 measured at
+# 1020 flop/clk/SM (tools/probe/mma_probe2.cu), 3 MMAs per product, 148 SMs at 1.965 GHz
+MMA_3XTF32_PEAK = 1020.0 / 3 * 148 * 1.965e9 / 1e12
+
+
 def roofline_peak():
     return FP32_PEAK_FALLBACK
 
@@ -377,8 +382,12 @@ def run_engine(args, rank, world):
                              "frac": achieved / peak, "traffic": k1_traffic(),
                              "traffic_unit": "bytes per launch (ncu dram__bytes_read+write)",
                              "algorithmic_bytes_per_launch": frames_per_launch * (4 * F + 8 * K),
-                             "kernel": ("solve_kernel (FP32 FMA + 3xTF32 mma.sync phase A)" if K <= 64 else
-                                        "solve_large_kernel (3xTF32 mma.sync, tensor pipe)"),
+                             "kernel": ("solve_mma_kernel (K1M: 3xTF32 mma.sync for every contraction)"
+                                        if K <= 56 and os.environ.get("ISNMF_MMA", "1") != "0" else
+                                        "solve_kernel (FP32 FMA + 3xTF32 mma.sync phase A)" if K <= 64 else
+                                        "solve_large_tc_kernel / solve_large_kernel (tcgen05 / mma.sync)"),
+                             "tensor_pipe_frac": achieved / MMA_3XTF32_PEAK,
+                             "tensor_pipe_peak": MMA_3XTF32_PEAK,
                              "ms_per_launch": k1_ms,
                              "flops_per_launch": flops_per_frame * frames_per_launch,
                              "k1_share_of_step": kstats["solve_ms"] / kstats["span_ms"],

@@ -22,7 +22,11 @@ want = ["gpu__time_duration.sum", "sm__throughput.avg.pct_of_peak_sustained_elap
         "smsp__issue_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
         "dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_bytes.sum", "launch__registers_per_thread",
         "sm__warps_active.avg.pct_of_peak_sustained_active", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
-        "smsp__sass_thread_inst_executed_op_ffma_pred_on.sum"]
+        "smsp__sass_thread_inst_executed_op_ffma_pred_on.sum",
+        "sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_tensor_subpipe_hmma.avg.pct_of_peak_sustained_active",
+        "sm__ops_path_tensor_src_tf32_dst_fp32.avg.pct_of_peak_sustained_elapsed",
+        "sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active"]
 for w in want:
     if w in h:
         print(f"{w:70s} {v[h.index(w)]}")
