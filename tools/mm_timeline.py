@@ -57,3 +57,7 @@ for w in range(nw):
         end = r[e + 4] if (e + 4 < 60 and r[e + 4] > r[e]) else r[61]
         out.append(f"{r[e + 1] - r[e]}/{r[e + 2] - r[e + 1]}/{r[e + 3] - r[e + 2]}/{end - r[e + 3]}")
     print(f"{w:3d}  " + "  ".join(out) + f"   (prep {r[44] - r[60]})")
+print("absolute stamps (cycles from CTA start) of passes 3-4: chunks-done / update-start / update-end")
+for w in range(nw):
+    r = ts[w]
+    print(f"{w:3d} grp{int(w >= nw // 2)}  " + "  ".join(f"{r[1 + 4 * p] - t0}/{r[2 + 4 * p] - t0}/{r[3 + 4 * p] - t0}" for p in (3, 4)))
