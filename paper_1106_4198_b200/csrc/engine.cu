@@ -139,6 +139,16 @@ cudaError_t launch_pdl(void (*fn)(P...), int grid, int block, size_t smem, cudaS
   return cudaLaunchKernelEx(&cfg, fn, std::forward<A>(args)...);
 }
 
+// growth factor of the host-frame chunk ramp (ISNMF_RAMP, A/B measurement only)
+double ramp_factor() {
+  static const double v = [] {
+    const char* e = getenv("ISNMF_RAMP");
+    const double r = e ? atof(e) : 1.125;
+    return r > 1.0 ? r : 1.125;
+  }();
+  return v;
+}
+
 int launch_fold(const FoldArgs& f, cudaStream_t s, bool pdl = false) {
   const size_t smem = fold_smem_bytes(f.F);
   if (smem + 1024 > size_t(smem_optin()))
@@ -751,11 +761,16 @@ int online_enqueue(isnmf_online* c, const float* frames, int64_t ldv, int64_t n,
   }
   int64_t pos = 0;
   int buf = 0;
-  // chunk sizes ramp up from two mini-batches so the first copy (not overlapped) is short
-  int64_t ramp = 2 * int64_t(c->beta);
+  // Chunk sizes ramp up from one mini-batch so the first copy (not overlapped) is short,
+  // growing by 1/8 per chunk (ramp_factor()): a copy of (9/8) s frames then takes about as long as the
+  // compute of the previous s frames (pinned H2D ~55 GB/s = ~0.9x the config-3 consumption
+  // rate), so the compute stream does not wait on the copy stream while the chunks grow
+  // (doubling made it wait ~9 ms per 2.7M-frame pass).
+  double ramp = double(c->beta);
   while (pos < n_eff) {
-    const int64_t cf = std::min<int64_t>(std::min<int64_t>(c->chunk, ramp), n_eff - pos);
-    ramp *= 2;
+    const int64_t rb = std::max<int64_t>(int64_t(c->beta), int64_t(ramp / c->beta) * c->beta);
+    const int64_t cf = std::min<int64_t>(std::min<int64_t>(c->chunk, rb), n_eff - pos);
+    ramp *= ramp_factor();
     CU(cudaStreamWaitEvent(c->xs, c->ev_free[buf], 0));
     if (ldv == c->F)  // contiguous frames: one linear DMA (2D copies run far below PCIe speed)
       CU(cudaMemcpyAsync(c->vbuf[buf], frames + pos * ldv, size_t(cf) * c->F * sizeof(float),
