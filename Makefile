@@ -5,23 +5,30 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v --expt-r
 PKG := paper_1106_4198_b200
 LIB := $(PKG)/lib/libisnmf_b200.so
 SRC := $(PKG)/csrc/engine.cu
+TABLES := $(PKG)/csrc/mma_table.cu $(PKG)/csrc/ffma_table.cu $(PKG)/csrc/large_table.cu
 DEPS := $(wildcard $(PKG)/csrc/*.cuh) include/isnmf_b200.h
+OBJ := $(PKG)/lib/engine.o $(PKG)/lib/mma_table.o $(PKG)/lib/ffma_table.o $(PKG)/lib/large_table.o
 
 all: $(LIB) oracle
 
-$(LIB): $(SRC) $(DEPS)
+# four translation units (the engine and three kernel-instantiation tables), compiled in parallel
+$(LIB): $(OBJ)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJ) -lcudart
+	@cat $(OBJ:.o=.ptxas.log) > $(PKG)/lib/ptxas.log
+
+$(PKG)/lib/%.o: $(PKG)/csrc/%.cu $(DEPS)
 	@mkdir -p $(PKG)/lib
-	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRC) -lcudart 2> $(PKG)/lib/ptxas.log || (cat $(PKG)/lib/ptxas.log; exit 1)
+	$(NVCC) $(NVFLAGS) -c -o $@ $< 2> $(PKG)/lib/$*.ptxas.log || (cat $(PKG)/lib/$*.ptxas.log; exit 1)
 
 oracle:
 	$(MAKE) -s -C oracle
 
 clean:
-	rm -rf $(PKG)/lib oracle/_build
+	rm -rf $(PKG)/lib $(PKG)/lib_prof oracle/_build oracle/_ref
 .PHONY: all oracle clean
 
 # experimental build with per-phase cycle counters (K1 headline variant only)
-prof: $(SRC) $(DEPS)
+prof: $(SRC) $(TABLES) $(DEPS)
 	@mkdir -p $(PKG)/lib_prof
-	$(NVCC) $(NVFLAGS) -DISNMF_PHASE_PROF -DISNMF_MIN_VARIANTS -shared -o $(PKG)/lib_prof/libisnmf_b200.so $(SRC) -lcudart 2> $(PKG)/lib_prof/ptxas.log || (cat $(PKG)/lib_prof/ptxas.log; exit 1)
+	$(NVCC) $(NVFLAGS) -DISNMF_PHASE_PROF -DISNMF_MIN_VARIANTS -shared -o $(PKG)/lib_prof/libisnmf_b200.so $(SRC) $(TABLES) -lcudart 2> $(PKG)/lib_prof/ptxas.log || (cat $(PKG)/lib_prof/ptxas.log; exit 1)
 .PHONY: prof

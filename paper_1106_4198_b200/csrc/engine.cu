@@ -29,6 +29,14 @@
 #include "kernels_mma.cuh"
 #include "stft.cuh"
 
+namespace isnmf_dev {
+// kernel instantiations in separate translation units (compiled in parallel):
+// K1M csrc/mma_table.cu, FFMA K1 csrc/ffma_table.cu, K1L / K1T csrc/large_table.cu
+void (*mma_kernel(int nw, int fg, int kb))(const SolveArgs);
+void (*ffma_kernel(int tk, int tn))(const SolveArgs);
+void (*large_kernel(int mbw, int nb))(const SolveArgs);
+void (*large_tc_kernel(int nb))(const SolveArgs);
+}  // namespace isnmf_dev
 using namespace isnmf_dev;
 
 namespace {
@@ -72,7 +80,7 @@ struct Variant {
   bool configured;
 };
 
-#define VAR(tk, tn) {tk, tn, solve_kernel<tk, tn>, &SolveShape<tk, tn>::smem_bytes, 0, false}
+#define VAR(tk, tn) {tk, tn, ffma_kernel(tk, tn), &SolveShape<tk, tn>::smem_bytes, 0, false}
 #ifdef ISNMF_MIN_VARIANTS  // fast experimental builds: the headline shape only
 Variant g_variants[] = {VAR(13, 7), VAR(5, 2), VAR(3, 1)};
 #else
@@ -204,10 +212,6 @@ int pick_variant(int64_t F, int64_t K, int64_t frames, Variant** out, int* WS, s
 // W fits shared memory, else the generic streaming kernel.
 // Tensor-pipe kernel for 64 < K <= 256 (config 4): [MBW - 1][NB - 1]
 using LargeFn = void (*)(const SolveArgs);
-#define LG(m, n) solve_large_kernel<m, n>
-LargeFn g_large[2][8] = {{LG(1, 1), LG(1, 2), LG(1, 3), LG(1, 4), LG(1, 5), LG(1, 6), LG(1, 7), LG(1, 8)},
-                         {LG(2, 1), LG(2, 2), LG(2, 3), LG(2, 4), LG(2, 5), LG(2, 6), LG(2, 7), LG(2, 8)}};
-#undef LG
 size_t large_smem(int mbw, int nb) {  // = LargeShape<mbw, nb>::smem_bytes()
   const int KP = 128 * mbw, NT = 8 * nb, FMB = (NT + 15) / 16;
   return sizeof(float) * (size_t(16 * FMB) * (KP + 4) + 3 * size_t(kLgChunk) * (KP + 4) + 2 * size_t(kLgChunk) * 136);
@@ -215,10 +219,7 @@ size_t large_smem(int mbw, int nb) {  // = LargeShape<mbw, nb>::smem_bytes()
 static_assert(LargeShape<2, 7>::smem_bytes() == sizeof(float) * (64 * 260 + 3 * 32 * 260 + 2 * 32 * 136),
               "large_smem() mirrors LargeShape::smem_bytes()");
 bool large_configured[2][8] = {};
-// tcgen05 variant (128 < K <= 256), [NB - 1]
-LargeFn g_large_tc[7] = {solve_large_tc_kernel<1>, solve_large_tc_kernel<2>, solve_large_tc_kernel<3>,
-                         solve_large_tc_kernel<4>, solve_large_tc_kernel<5>, solve_large_tc_kernel<6>,
-                         solve_large_tc_kernel<7>};
+// tcgen05 variant (128 < K <= 256): large_tc_kernel(nb)
 size_t large_tc_smem(int nb) {
   switch (nb) {
     case 1: return LargeTcShape<1>::smem_bytes();
@@ -239,12 +240,7 @@ bool tc_enabled() {
   return on;
 }
 
-// K1M: all-tensor-pipe solve for K <= 56, [NW == 12][FG - 1][KB - 1]
-#define MM(kb, fg, nw) solve_mma_kernel<kb, fg, nw>
-#define MMROW(fg, nw) {MM(1, fg, nw), MM(2, fg, nw), MM(3, fg, nw), MM(4, fg, nw), MM(5, fg, nw), MM(6, fg, nw), MM(7, fg, nw)}
-LargeFn g_mma[2][2][7] = {{MMROW(1, 8), MMROW(2, 8)}, {MMROW(1, 12), MMROW(2, 12)}};
-#undef MMROW
-#undef MM
+// K1M: all-tensor-pipe solve for K <= 56 (instantiated in csrc/mma_table.cu)
 size_t mma_smem(int kb, int fg, int nw, int F) {
   const int KP = 8 * kb, NT = 16 * fg, WS = mm_stride(KP), HT = mm_stride(NT);
   const size_t F16 = size_t((F + 15) & ~15), red = size_t(nw) * 8 * kb * 32, ht = size_t(KP) * HT;
@@ -296,11 +292,11 @@ int plan_solve(int64_t F, int64_t K, int64_t frames, SolvePlan* plan, bool force
     const int wi = nw == 12 ? 1 : 0;
     if (nt >= mma_min_frames() && smem + 2048 <= size_t(smem_optin())) {
       if (!mma_configured[wi][fg - 1][kb - 1]) {
-        CU(cudaFuncSetAttribute(g_mma[wi][fg - 1][kb - 1], cudaFuncAttributeMaxDynamicSharedMemorySize,
+        CU(cudaFuncSetAttribute(mma_kernel(nw, fg, kb), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 smem_optin() - 2048));
         mma_configured[wi][fg - 1][kb - 1] = true;
       }
-      plan->large = g_mma[wi][fg - 1][kb - 1];
+      plan->large = mma_kernel(nw, fg, kb);
       plan->threads = 32 * nw;
       plan->var = nullptr;
       plan->NT = nt;
@@ -328,11 +324,11 @@ int plan_solve(int64_t F, int64_t K, int64_t frames, SolvePlan* plan, bool force
       const size_t smem = large_tc_smem(nb);
       if (smem + 2048 <= size_t(smem_optin())) {
         if (!large_tc_configured[nb - 1]) {
-          CU(cudaFuncSetAttribute(g_large_tc[nb - 1], cudaFuncAttributeMaxDynamicSharedMemorySize,
+          CU(cudaFuncSetAttribute(large_tc_kernel(nb), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   smem_optin() - 2048));
           large_tc_configured[nb - 1] = true;
         }
-        plan->large = g_large_tc[nb - 1];
+        plan->large = large_tc_kernel(nb);
         plan->threads = kTcThreads;
         plan->var = nullptr;
         plan->NT = 8 * nb;
@@ -345,11 +341,11 @@ int plan_solve(int64_t F, int64_t K, int64_t frames, SolvePlan* plan, bool force
     const size_t smem = large_smem(mbw, nb);
     if (smem + 2048 <= size_t(smem_optin())) {
       if (!large_configured[mbw - 1][nb - 1]) {
-        CU(cudaFuncSetAttribute(g_large[mbw - 1][nb - 1], cudaFuncAttributeMaxDynamicSharedMemorySize,
+        CU(cudaFuncSetAttribute(large_kernel(mbw, nb), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 smem_optin() - 2048));
         large_configured[mbw - 1][nb - 1] = true;
       }
-      plan->large = g_large[mbw - 1][nb - 1];
+      plan->large = large_kernel(mbw, nb);
       plan->threads = kLgThreads;
       plan->var = nullptr;
       plan->NT = 8 * nb;

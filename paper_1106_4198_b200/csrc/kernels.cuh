@@ -986,6 +986,7 @@ __device__ __forceinline__ double block_sum_d(double v, double* red) {
   return s;
 }
 
+#ifndef ISNMF_TEMPLATES_ONLY  // defined once, in engine.cu's translation unit
 __global__ void __cluster_dims__(kFoldCluster, 1, 1) __launch_bounds__(kFoldThreads)
     fold_commit_kernel(const FoldArgs a) {
   pdl_trigger();  // the next K1 may start its launch; it waits for this grid before touching its outputs
@@ -1214,6 +1215,7 @@ __global__ void __cluster_dims__(kFoldCluster, 1, 1) __launch_bounds__(kFoldThre
   }
   FOLD_T(7);
 }
+#endif
 
 // ---------------------------------------------------------------------------
 // K0 — std::mt19937_64 (libstdc++ algorithm) per frame for fresh restarts.
@@ -1225,6 +1227,7 @@ __device__ __forceinline__ uint64_t splitmix64_d(uint64_t x) {
   return x ^ (x >> 31);
 }
 
+#ifndef ISNMF_TEMPLATES_ONLY  // defined once, in engine.cu's translation unit
 __global__ void fresh_kernel(uint64_t seed, uint64_t t0, int n, int K, double* u01) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -1259,6 +1262,7 @@ __global__ void fresh_kernel(uint64_t seed, uint64_t t0, int n, int K, double* u
     u01[size_t(i) * K + k] = 1.0 - double(z >> 11) * 0x1.0p-53;  // uniform_open01 (rng.hpp:27-34)
   }
 }
+#endif
 
 }  // namespace isnmf_dev
 
@@ -1282,6 +1286,7 @@ struct GenShape {
   __host__ __device__ size_t smem_floats() const { return size_t(NT) * KP + size_t(kGenChunk) * WS + size_t(kGenChunk) * QS; }
 };
 
+#ifndef ISNMF_TEMPLATES_ONLY  // defined once, in engine.cu's translation unit
 __global__ void __launch_bounds__(kGenThreads, 1) solve_generic_kernel(const SolveArgs a, int NT) {
   if (*a.status || (a.halt && *a.halt)) return;
   const int F = a.F, K = a.K;
@@ -1448,5 +1453,6 @@ __global__ void __launch_bounds__(kGenThreads, 1) solve_generic_kernel(const Sol
     }
   }
 }
+#endif
 
 }  // namespace isnmf_dev
