@@ -147,14 +147,20 @@ cudaError_t launch_pdl(void (*fn)(P...), int grid, int block, size_t smem, cudaS
   return cudaLaunchKernelEx(&cfg, fn, std::forward<A>(args)...);
 }
 
-// growth factor of the host-frame chunk ramp (ISNMF_RAMP, A/B measurement only)
-double ramp_factor() {
-  static const double v = [] {
+// Growth factor of the host-frame chunk ramp.  A chunk of r*s frames must copy in
+// about the compute time of the previous s frames: copy/compute per frame is
+// ~ (4F B / 50 GB/s) / (6FK(I+1) flop / 45 TFLOP/s) = 600 / (K (I+1)), so r =
+// 0.95 (K (I+1)) / 600, clamped to [1.125, 4] (config 3: 1.125; config 4: 3.6 —
+// each chunk boundary also costs time, so compute-heavy shapes grow fast).
+// ISNMF_RAMP overrides it (A/B measurement only).
+double ramp_factor(int K, int iters) {
+  static const double env = [] {
     const char* e = getenv("ISNMF_RAMP");
-    const double r = e ? atof(e) : 1.125;
-    return r > 1.0 ? r : 1.125;
+    return e ? atof(e) : 0.0;
   }();
-  return v;
+  if (env > 1.0) return env;
+  const double r = 0.95 * double(K) * double(iters + 1) / 600.0;
+  return r < 1.125 ? 1.125 : (r > 4.0 ? 4.0 : r);
 }
 
 int launch_fold(const FoldArgs& f, cudaStream_t s, bool pdl = false) {
@@ -758,15 +764,15 @@ int online_enqueue(isnmf_online* c, const float* frames, int64_t ldv, int64_t n,
   int64_t pos = 0;
   int buf = 0;
   // Chunk sizes ramp up from one mini-batch so the first copy (not overlapped) is short,
-  // growing by 1/8 per chunk (ramp_factor()): a copy of (9/8) s frames then takes about as long as the
-  // compute of the previous s frames (pinned H2D ~55 GB/s = ~0.9x the config-3 consumption
-  // rate), so the compute stream does not wait on the copy stream while the chunks grow
-  // (doubling made it wait ~9 ms per 2.7M-frame pass).
+  // growing by ramp_factor() per chunk: at config 3 (1/8) a copy of 9/8 s frames takes
+  // about as long as the compute of the previous s frames (pinned H2D ~55 GB/s = ~0.9x
+  // the consumption rate), so the compute stream does not wait on the copy stream while
+  // the chunks grow (doubling made it wait ~9 ms per 2.7M-frame pass).
   double ramp = double(c->beta);
   while (pos < n_eff) {
     const int64_t rb = std::max<int64_t>(int64_t(c->beta), int64_t(ramp / c->beta) * c->beta);
     const int64_t cf = std::min<int64_t>(std::min<int64_t>(c->chunk, rb), n_eff - pos);
-    ramp *= ramp_factor();
+    ramp *= ramp_factor(c->K, c->iters);
     CU(cudaStreamWaitEvent(c->xs, c->ev_free[buf], 0));
     if (ldv == c->F)  // contiguous frames: one linear DMA (2D copies run far below PCIe speed)
       CU(cudaMemcpyAsync(c->vbuf[buf], frames + pos * ldv, size_t(cf) * c->F * sizeof(float),
