@@ -37,7 +37,6 @@
 
 namespace isnmf_dev {
 
-constexpr int kMmWarpsMax = 12;
 
 // smallest stride >= n (a multiple of 8) that is 8 or 24 mod 32 words: the
 // 64-bit fragment loads of a half warp (8-word groups of 4 rows) hit 32 banks
