@@ -402,6 +402,8 @@ __global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a
   __shared__ const float* fptr[NT];
   __shared__ double red[kMmThreads / 32];
   __shared__ double meanv[NT];
+  __shared__ int64_t colv[NT];  // warm store column of each frame
+  __shared__ uint32_t tagv[NT];  // and its commit tag
   __shared__ int s_bad;
   __shared__ __align__(8) unsigned long long wbar;
 
@@ -430,6 +432,11 @@ __global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a
   if (tid < NT) {
     const int64_t fr = tid < nf ? (a.vsel ? a.vsel[n0 + tid] : a.v0 + n0 + tid) : 0;
     fptr[tid] = a.V + fr * a.ldv;
+    if (a.h0_mode == 1 && tid < nf) {  // per-frame warm-store column and tag, off the per-element chain
+      const int64_t col = a.widx ? int64_t(a.widx[n0 + tid]) : (a.wbase + n0 + tid) % a.wmod;
+      colv[tid] = col;
+      tagv[tid] = a.T[col];
+    }
   }
   if (tid == 0) s_bad = 0;
   __syncthreads();
@@ -450,9 +457,8 @@ __global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a
       if (a.h0_mode == 0) {
         val = a.H0[size_t(n0 + n) * K + k];
       } else if (a.h0_mode == 1) {
-        const int64_t col = a.widx ? int64_t(a.widx[n0 + n]) : (a.wbase + n0 + n) % a.wmod;
-        const uint32_t tag = a.T[col];
-        const double ratio = a.P[size_t(a.c_now) * K + k] / a.P[size_t(tag) * K + k];
+        const int64_t col = colv[n];
+        const double ratio = a.P[size_t(a.c_now) * K + k] / a.P[size_t(tagv[n]) * K + k];
         val = float(double(a.U[size_t(col) * K + k]) * ratio);
       } else {
         const double mv = meanv[n] > a.epsd ? meanv[n] : a.epsd;
