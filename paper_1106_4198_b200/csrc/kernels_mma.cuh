@@ -388,7 +388,9 @@ __global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a
   using S = MmShape<KB, FG, NW>;
   constexpr int KP = S::KP, NT = S::NT, RG = S::RG, WS = S::WS, HT = S::HT, NREG = S::NREG;
   constexpr int kMmThreads = 32 * NW;
+  MM_STAMP(62);
   pdl_wait();
+  MM_STAMP(58);
   if (*a.status || (a.halt && *a.halt)) return;
 
   extern __shared__ __align__(16) float smem[];
@@ -638,6 +640,7 @@ __global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a
       }
     }
   }
+  MM_STAMP(63);
 }
 
 }  // namespace isnmf_dev

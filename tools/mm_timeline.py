@@ -30,7 +30,7 @@ nw = 12
 buf = np.zeros(4096, dtype=np.int64)
 L.isnmf_debug_phase_prof(eng._h, buf.ctypes.data_as(C.c_void_p), buf.size, 0)
 ts = buf[: nw * 64].reshape(nw, 64).astype(np.int64)
-t0 = ts[:, 0].min()
+t0 = ts[:, 62].min()
 print("warp  prologue  " + "  ".join(f"p{p}:mma/bar1/upd/bar2" for p in range(3)) + "  ...  stats  total")
 tot = np.zeros(4)
 for w in range(nw):
@@ -61,3 +61,8 @@ print("absolute stamps (cycles from CTA start) of passes 3-4: chunks-done / upda
 for w in range(nw):
     r = ts[w]
     print(f"{w:3d} grp{int(w >= nw // 2)}  " + "  ".join(f"{r[1 + 4 * p] - t0}/{r[2 + 4 * p] - t0}/{r[3 + 4 * p] - t0}" for p in (3, 4)))
+print("prologue (entry -> passes) / stats end -> exit, cycles:")
+for w in range(nw):
+    r = ts[w]
+    print(f"{w:3d}  entry {r[62] - t0:7d}  pdl wait {r[58] - r[62]:6d}  prologue {r[0] - r[58]:6d}  "
+          f"stats prep {r[44] - r[60]:6d}  epilogue {r[63] - r[61]:6d}  exit {r[63] - t0:7d}")
