@@ -12,6 +12,10 @@
 // and ~10x fewer issued instructions than FFMA register tiles, which is what
 // bounded the FFMA kernel (issue-limited at ~55%).
 //
+// CTA: NW = 12 warps (8 when shared memory is short) = FG frame groups x RG row
+// groups; W resident in shared memory (TMA bulk load, rows padded to 16 with zeros);
+// h kept only as a pre-split fragment copy ([fm][kb][hi | lo][lane][4]).
+//
 // Iterations: warp (fm, rq) owns frames [16fm, 16fm+16) and the rq-th share of
 // the dictionary rows in 8-row blocks; per chunk of up to 4 blocks
 //   phase A  Lam^T[frame][row] = h^T W^T        (M = 16 frames, N = 8 rows, K = k)
@@ -24,7 +28,8 @@
 // rho(g) = g ^ (g >> 2)) so that both phases' dictionary loads are free of
 // bank conflicts with a row stride of 8 or 24 mod 32 words.  The RG warps of a
 // frame group sum their num/den partials in a fixed order through shared memory
-// (bitwise reproducible), then h *= sqrt(num/den).
+// (bitwise reproducible), then h *= sqrt(num/den); each group synchronises on its
+// own named barrier, and every SM sub-partition hosts warps of both groups.
 //
 // Statistics pass (final h): warps own 16-row blocks and all frames,
 //   Lam[row][frame] = W h                      (M = 16 rows, N = 8 frames, K = k)
