@@ -378,7 +378,10 @@ def run_engine(args, rank, world):
                                        f"rho={rho:.6f}, warm store h0=1, 1 pass per step",
                            "global_batch": beta, "parallelism": "replicas" if world > 1 else "single",
                            "l2": "inputs larger than L2 (V = %.2f GB fp32)" % (N * F * 4 / 1e9)},
-                "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "roofline": {"bound": "fp32", "bound_note": "north_star roofline: the pass's flops at the FP32 FMA "
+                                                    "peak (compute bound, ~690 flop/B); K1M computes on the HMMA "
+                                                    "pipe, whose 3xTF32 ceiling is tensor_pipe_peak",
+                             "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                              "frac": achieved / peak, "traffic": k1_traffic(),
                              "traffic_unit": "bytes per launch (ncu dram__bytes_read+write)",
                              "algorithmic_bytes_per_launch": frames_per_launch * (4 * F + 8 * K),
