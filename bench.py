@@ -41,7 +41,10 @@ sys.path.insert(0, os.path.join(ROOT, "oracle"))
 from tools.synth import CONFIGS  # noqa: E402
 
 MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
-FP32_PEAK_FALLBACK = 72.4  # TFLOP/s, tools/probe measured on this pool (profiles/r01_probe.txt)
+# FP32 FMA peak: MEASURED_PEAKS.json carries no FP32 figure, so the denominator is the
+# nominal 148 SM x 128 lanes x 2 flop x 1.965 GHz (clocks.max.sm) — the highest the
+# part can issue; tools/probe measured 72.4 on this pool (profiles/r01_probe.txt)
+FP32_PEAK_NOMINAL = 148 * 128 * 2 * 1.965e9 / 1e12
 
 
 def parse(argv=None):
@@ -154,17 +157,14 @@ def dist_done(world):
 MMA_3XTF32_PEAK = 1020.0 / 3 * 148 * 1.965e9 / 1e12
 
 
-def roofline_peak():
-    return FP32_PEAK_FALLBACK
-
-
-def k1_traffic():
-    """DRAM bytes per K1 launch from the committed ncu --set full capture (or None)."""
+def k1_traffic(config):
+    """DRAM bytes per K1 launch of this config from its committed ncu --set full
+    capture (profiles/k1_traffic_<config>.json), or None when there is none."""
     try:
-        d = json.load(open(os.path.join(ROOT, "profiles", "k1_traffic.json")))
-        return d["dram_bytes_read"] + d["dram_bytes_write"]
+        d = json.load(open(os.path.join(ROOT, "profiles", f"k1_traffic_{config}.json")))
+        return d["dram_bytes_read"] + d["dram_bytes_write"], d.get("source")
     except (OSError, ValueError, KeyError):
-        return None
+        return None, None
 
 
 def cpu_baseline(cfg, v_host_cols, w0, a0, threads, batches):
@@ -285,44 +285,54 @@ def run_engine(args, rank, world):
     a0 = np.full((F, K), 1e-3)
 
     eng = E.Online(F, K, beta, iters, restart="warm", n_store=N)
-    eng.set_dictionary(w0, a0, a0)
-    eng.set_counters(0, 0, rho)
-    eng.fill_warm_h(1.0)
-    L = E.lib()
+
+    def reinit():
+        """Config 3's initial state (W0, A0 = B0 = 1e-3, t = commits = 0, warm store
+        h0 = 1): every step is exactly one config-3 pass, not a continuation."""
+        eng.set_dictionary(w0, a0, a0)
+        eng.set_counters(0, 0, rho)
+        eng.fill_warm_h(1.0)
 
     def one_pass(frames):
         eng.enqueue(frames, N, frames.stride(0))
 
     # warm-up
     for _ in range(args.warmup):
+        reinit()
         one_pass(vd)
-    eng.synchronize()
+        eng.synchronize()
 
-    # timed region: K passes, V resident in HBM.  Device time = CUDA events on
-    # the engine's own compute stream (every engine kernel runs there), bracketed
-    # by a barrier + device synchronize on both sides.
-    launches0 = eng.launch_count()
-    prof = E.Profile(eng, per_kernel=False)  # events only around the region (per-kernel events cost ~1%)
+    # timed steps: V resident in HBM.  Each step re-initialises the state outside
+    # the timed region, then one pass is bracketed by a barrier + device
+    # synchronize on both sides and timed with CUDA events on the engine's own
+    # compute stream (every engine kernel runs there); value = frames / the sum of
+    # the step times (max over ranks).
+    launches = 0
+    ms_total = 0.0
+    wall = 0.0
     with ClockSampler(dev) as clk:
         time.sleep(0.5)  # let nvidia-smi start sampling before the timed region
-        barrier(world)
-        torch.cuda.synchronize()
-        prof.start()
-        t_wall = time.perf_counter()
         for _ in range(args.steps):
+            reinit()
+            barrier(world)
+            torch.cuda.synchronize()
+            launches0 = eng.launch_count()
+            prof = E.Profile(eng, per_kernel=False)  # events only around the step (per-kernel events cost ~1%)
+            prof.start()
+            t_wall = time.perf_counter()
             one_pass(vd)
-        eng.synchronize()
-        kstats = prof.stop()
-        torch.cuda.synchronize()
-        wall = time.perf_counter() - t_wall
-        barrier(world)
-    ms_total = kstats["span_ms"]
-    launches = eng.launch_count() - launches0
-    ms_total = allmax(ms_total, world)
+            eng.synchronize()
+            kstats = prof.stop()
+            torch.cuda.synchronize()
+            wall += time.perf_counter() - t_wall
+            barrier(world)
+            ms_total += allmax(kstats["span_ms"], world)
+            launches += eng.launch_count() - launches0
     value = world * N * args.steps / (ms_total / 1e3)
     st = eng.state()
 
     # roofline of K1: one more pass with events around every launch (not part of `value`)
+    reinit()
     kprof = E.Profile(eng, per_kernel=True)
     kprof.start()
     one_pass(vd)
@@ -332,28 +342,35 @@ def run_engine(args, rank, world):
     frames_per_launch = kstats["solve_frames"] / max(1, kstats["solve_launches"])
     k2_ms = kstats["tail_ms"] / max(1, kstats["solve_launches"])
     achieved = flops_per_frame * frames_per_launch / (k1_ms / 1e3) / 1e12
-    peak = roofline_peak()
+    peak = FP32_PEAK_NOMINAL
 
-    # e2e: same call with host (pinned) frames, W read back every step
+    # e2e: the whole user call through the C ABI with V in pinned HOST memory —
+    # initial state pushed (W0/A0/B0 H2D, store fill), the pass (V streamed H2D in
+    # chunks on the copy stream, double-buffered), the dictionary read back (D2H)
     e2e = None
     if not args.no_e2e:
         vh = torch.empty_like(vd, device="cpu").pin_memory()
         vh.copy_(vd)
         del vd
         torch.cuda.empty_cache()
+        reinit()
         one_pass(vh)
         eng.synchronize()
         wbuf = np.empty((F, K), order="F")
-        barrier(world)
-        t0 = time.perf_counter()
+        e2e_s = 0.0
         for _ in range(args.steps):
+            barrier(world)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            reinit()
             one_pass(vh)
             eng.synchronize()
             E.lib().isnmf_online_get_dictionary(eng._h, E._p(wbuf), None, None)
-        e2e_s = allmax(time.perf_counter() - t0, world)
+            e2e_s += allmax(time.perf_counter() - t0, world)
         e2e = {"value": world * N * args.steps / e2e_s, "unit": "frames/s",
-               "h2d_bytes_per_step": int(N * F * 4), "d2h_bytes_per_step": int(F * K * 8),
-               "h2d_gbs": N * F * 4 * args.steps / e2e_s / 1e9}
+               "h2d_bytes_per_step": int(N * F * 4 + 3 * F * K * 8), "d2h_bytes_per_step": int(F * K * 8),
+               "h2d_gbs": N * F * 4 * args.steps / e2e_s / 1e9,
+               "timing": "host wall clock per step (state init + pass + W read back), summed over steps"}
 
     cpu = None
     if rank == 0 and not args.no_cpu:
@@ -367,6 +384,7 @@ def run_engine(args, rank, world):
                          f"fp64 oracle restatement of the reference path on 1 core of {cpu_name} "
                          f"({ncpu} cores); the reference itself cannot be compiled (no Eigen)"}
 
+    traffic, traffic_src = k1_traffic(args.config)
     if rank == 0:
         metric = ("online IS-NMF frames/sec (F=513,K=50,beta=4096)" if args.config == "c3" else
                   f"online IS-NMF frames/sec ({args.config}: F={F},K={K},beta={beta})")
@@ -375,14 +393,15 @@ def run_engine(args, rank, world):
                 "ms_per_step": ms_total / args.steps, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "config": {"workload": f"{args.config}: F={F}, K={K}, beta={beta}, I={iters}, N={N}, "
-                                       f"rho={rho:.6f}, warm store h0=1, 1 pass per step",
+                                       f"rho={rho:.6f}; each step = one pass from W0, A0=B0=1e-3, "
+                                       f"warm store h0=1 (state re-initialised outside the timed region)",
                            "global_batch": beta, "parallelism": "replicas" if world > 1 else "single",
                            "l2": "inputs larger than L2 (V = %.2f GB fp32)" % (N * F * 4 / 1e9)},
                 "roofline": {"bound": "fp32", "bound_note": "north_star roofline: the pass's flops at the FP32 FMA "
                                                     "peak (compute bound, ~690 flop/B); K1M computes on the HMMA "
                                                     "pipe, whose 3xTF32 ceiling is tensor_pipe_peak",
                              "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                             "frac": achieved / peak, "traffic": k1_traffic(),
+                             "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                              "traffic_unit": "bytes per launch (ncu dram__bytes_read+write)",
                              "algorithmic_bytes_per_launch": frames_per_launch * (4 * F + 8 * K),
                              "kernel": ("solve_mma_kernel (K1M: 3xTF32 mma.sync for every contraction)"
@@ -396,8 +415,9 @@ def run_engine(args, rank, world):
                              "k1_share_of_step": kstats["solve_ms"] / kstats["span_ms"],
                              "k2_us_per_minibatch": 1e3 * k2_ms,
                              "pass_frac": flops_per_frame * N * args.steps / (ms_total / 1e3) / 1e12 / peak,
-                             "peak_source": "FP32 FMA peak measured by tools/probe on this pool (72.4 TFLOP/s); "
-                                            "nominal 148 SM x 128 x 2 x 1.965 GHz = 74.4"},
+                             "peak_source": "nominal FP32 FMA peak 148 SM x 128 x 2 x 1.965 GHz = 74.4 TFLOP/s "
+                                            "(MEASURED_PEAKS.json has no FP32 entry; tools/probe measured 72.4 "
+                                            "on this pool)"},
                 "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches,
                 "clocks": clk.summary(), "wall_s": wall,
                 "final": {"t": st["t"], "commits": st["commits"], "last_minibatch_obj": st["last_minibatch_obj"]}}

@@ -427,10 +427,6 @@ bool is_device_ptr(const void* p) {
   return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
 }
 
-__global__ void fill_f32(float* p, int64_t n, float v) {
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
-    p[i] = v;
-}
 __global__ void fill_u32(uint32_t* p, int64_t n, uint32_t v) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
     p[i] = v;
@@ -440,21 +436,20 @@ __global__ void fill_f64(double* p, int64_t n, double v) {
     p[i] = v;
 }
 // U[col] <- current value (U * P[c]/P[T]), T <- c_new.
-__global__ void warm_rebase(float* U, uint32_t* T, const double* P, int64_t n, int K, uint32_t c_old,
+__global__ void warm_rebase(double* U, uint32_t* T, const double* P, int64_t n, int K, uint32_t c_old,
                             uint32_t c_new) {
   for (int64_t col = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; col < n; col += int64_t(gridDim.x) * blockDim.x) {
     const uint32_t tag = T[col];
-    for (int k = 0; k < K; ++k)
-      U[col * K + k] = float(double(U[col * K + k]) * (P[size_t(c_old) * K + k] / P[size_t(tag) * K + k]));
+    for (int k = 0; k < K; ++k) U[col * K + k] *= P[size_t(c_old) * K + k] / P[size_t(tag) * K + k];
     T[col] = c_new;
   }
 }
-__global__ void warm_read(const float* U, const uint32_t* T, const double* P, int64_t n, int K, uint32_t c,
+__global__ void warm_read(const double* U, const uint32_t* T, const double* P, int64_t n, int K, uint32_t c,
                           double* out) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n * K; i += int64_t(gridDim.x) * blockDim.x) {
     const int64_t col = i / K;
     const int k = int(i - col * K);
-    out[i] = double(U[i]) * (P[size_t(c) * K + k] / P[size_t(T[col]) * K + k]);
+    out[i] = U[i] * (P[size_t(c) * K + k] / P[size_t(T[col]) * K + k]);
   }
 }
 __global__ void mark_origin(DevState* st) { st->origin_ns = globaltimer_ns(); }
@@ -490,7 +485,7 @@ struct isnmf_online {
   float* stats = nullptr;
   double* divpart = nullptr;
   int maxblk = 0;
-  float* U = nullptr;
+  double* U = nullptr;  // warm activation store (fp64, see kernels.cuh warm_value)
   uint32_t* T = nullptr;
   int64_t nstore = 0;
   double* u01 = nullptr;
@@ -799,7 +794,14 @@ int online_finish(isnmf_online* c, int32_t* stopped) {
   c->t_host = h.t;
   c->commits_host = h.commits;
   if (stopped) *stopped = int32_t(h.halt != 0);
-  if (h.status) return status_to_code(h.status, "online", h.t);
+  if (h.status) {
+    // report once, then clear: the reference's exceptions leave the state usable
+    // (solve_h throws before it mutates anything), so the context must be too
+    const unsigned int zero = 0;
+    CU(cudaMemcpy(reinterpret_cast<char*>(c->st) + offsetof(DevState, status), &zero, sizeof(zero),
+                  cudaMemcpyHostToDevice));
+    return status_to_code(h.status, "online", h.t);
+  }
   return 0;
 }
 
@@ -887,7 +889,7 @@ int isnmf_online_create(isnmf_online** out, const isnmf_online_config* cfg) {
   if ((rc = settle())) return bail(rc);
   fill_f64<<<64, 256, 0, c->cs>>>(c->P, c->Pcap * c->K, 1.0);
   if (c->restart == ISNMF_RESTART_WARM) {
-    fill_f32<<<592, 256, 0, c->cs>>>(c->U, c->nstore * c->K, 1.0f);
+    fill_f64<<<592, 256, 0, c->cs>>>(c->U, c->nstore * c->K, 1.0);
     fill_u32<<<592, 256, 0, c->cs>>>(c->T, c->nstore, 0u);
   }
   mark_origin<<<1, 1, 0, c->cs>>>(c->st);
@@ -1011,10 +1013,8 @@ int isnmf_online_get_counters(isnmf_online* c, uint64_t* t, uint64_t* commits, d
 int isnmf_online_set_warm_h(isnmf_online* c, const double* warm_h) {
   if (!c || !warm_h) return fail(ISNMF_E_INVALID_ARG, "NULL argument");
   if (c->restart != ISNMF_RESTART_WARM) return fail(ISNMF_E_INVALID_ARG, "set_warm_h: context is not warm");
-  std::vector<float> u(size_t(c->nstore) * c->K);
-  for (size_t i = 0; i < u.size(); ++i) u[i] = float(warm_h[i]);
   CU(cudaStreamSynchronize(c->cs));
-  CU(cudaMemcpy(c->U, u.data(), u.size() * sizeof(float), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(c->U, warm_h, size_t(c->nstore) * c->K * sizeof(double), cudaMemcpyHostToDevice));
   TRY(settle());
   fill_u32<<<592, 256, 0, c->cs>>>(c->T, c->nstore, uint32_t(c->commits_host));
   fill_f64<<<1, 256, 0, c->cs>>>(c->P + size_t(c->commits_host) * c->K, c->K, 1.0);
@@ -1025,7 +1025,7 @@ int isnmf_online_set_warm_h(isnmf_online* c, const double* warm_h) {
 int isnmf_online_fill_warm_h(isnmf_online* c, double value) {
   if (!c) return fail(ISNMF_E_INVALID_ARG, "NULL context");
   if (c->restart != ISNMF_RESTART_WARM) return fail(ISNMF_E_INVALID_ARG, "fill_warm_h: context is not warm");
-  fill_f32<<<592, 256, 0, c->cs>>>(c->U, c->nstore * c->K, float(value));
+  fill_f64<<<592, 256, 0, c->cs>>>(c->U, c->nstore * c->K, value);
   fill_u32<<<592, 256, 0, c->cs>>>(c->T, c->nstore, uint32_t(c->commits_host));
   fill_f64<<<1, 256, 0, c->cs>>>(c->P + size_t(c->commits_host) * c->K, c->K, 1.0);
   CU(cudaStreamSynchronize(c->cs));

@@ -137,7 +137,7 @@ struct SolveArgs {
   double epsd;
   int h0_mode;  // 0 direct H0, 1 warm store (U, T, P), 2 fresh (u01, kmeanw)
   const float* H0;
-  float* U;
+  double* U;
   uint32_t* T;
   const double* P;
   uint32_t c_now;
@@ -158,6 +158,80 @@ struct SolveArgs {
   const unsigned int* halt;
   long long* prof;  // phase cycle counters (ISNMF_PHASE_PROF builds only)
 };
+
+// ---------------------------------------------------------------------------
+// Warm activation store — the reference's fp64 warm_h (online.hpp:229, 348-358).
+// U[col][k] is fp64, T[col] the commit at which column col was last written; its
+// value now is U * P[c_now][k] / P[T][k] (P = prefix products of the column
+// scales, so the rescale of every stored H at each commit, model.hpp:84, costs
+// O(K)).  The solver works in fp32, whose range does not cover every value the
+// fp64 reference keeps: an atom that a frame does not use decays geometrically
+// under the MM update, visit after visit (fp32 would flush it to 0 and the next
+// visit would raise NonPositiveInit where the reference does not).  Such an h
+// enters the solver as kWarmFloor — W * 2^-80 is ~1e-12 of the smallest Lam
+// (eps = 1e-12) and leaves Lam's fp32 value unchanged, so the update factors
+// sqrt(num/den) are the ones the true value sees — and the store keeps
+// h0 * (h / kWarmFloor) in fp64.
+// ---------------------------------------------------------------------------
+constexpr float kWarmFloor = 0x1p-80f;
+
+__device__ __forceinline__ int64_t warm_col(const SolveArgs& a, int n) {  // n = launch-local frame
+  return a.widx ? int64_t(a.widx[n]) : (a.wbase + n) % a.wmod;
+}
+__device__ __forceinline__ double warm_value(const SolveArgs& a, int64_t col, uint32_t tag, int k) {
+  return a.U[size_t(col) * a.K + k] * (a.P[size_t(a.c_now) * a.K + k] / a.P[size_t(tag) * a.K + k]);
+}
+
+// h0 of launch-local frame n, atom k (n < nframes, k < K) as the solver's fp32
+// start value; sets bad when the reference's solve_h would raise NonPositiveInit
+// (h0 <= 0 or NaN, kernels.hpp:67).  meanv = the frame's mean (fresh mode only).
+__device__ __forceinline__ float solve_h0(const SolveArgs& a, int n, int k, int64_t col, uint32_t tag,
+                                          double meanv, int& bad) {
+  float val;
+  if (a.h0_mode == 1) {
+    const double h0 = warm_value(a, col, tag, k);
+    if (!(h0 > 0.0)) bad = 1;
+    val = h0 < double(kWarmFloor) && h0 > 0.0 ? kWarmFloor : float(h0);
+  } else {
+    if (a.h0_mode == 0) {
+      val = a.H0[size_t(n) * a.K + k];
+    } else {
+      const double mv = meanv > a.epsd ? meanv : a.epsd;
+      val = float(mv / a.kst->kmeanw * a.u01[size_t(n) * a.K + k]);
+    }
+    if (a.hscale) val = float(double(val) * a.hscale[k]);
+    if (!(val > 0.0f)) bad = 1;
+  }
+  return val;
+}
+
+// Writes the final h of atom k to store column col (tag = the column's tag when
+// the launch started; T is re-tagged separately, after every U write of the CTA).
+__device__ __forceinline__ void warm_put(const SolveArgs& a, int64_t col, uint32_t tag, int k, float h) {
+  const double h0 = warm_value(a, col, tag, k);
+  a.U[size_t(col) * a.K + k] = h0 < double(kWarmFloor) ? h0 * (double(h) / double(kWarmFloor)) : double(h);
+}
+
+// Epilogue of every K1 variant: Hout and the warm store for the CTA's frames
+// [n0, n0 + nf); hval(n, k) reads the final h.  Every thread of the CTA calls it.
+template <class HVal>
+__device__ __forceinline__ void write_final_h(const SolveArgs& a, int n0, int nf, HVal hval) {
+  if (!a.Hout && !a.write_store) return;
+  const int K = a.K;
+  for (int idx = threadIdx.x; idx < nf * K; idx += blockDim.x) {
+    const int n = idx / K, k = idx - n * K;
+    const float h = hval(n, k);
+    if (a.Hout) a.Hout[size_t(n0 + n) * K + k] = h;
+    if (a.write_store) {
+      const int64_t col = warm_col(a, n0 + n);
+      warm_put(a, col, a.T[col], k, h);
+    }
+  }
+  if (a.write_store) {
+    __syncthreads();  // every U write of this CTA has read its column's old tag
+    for (int n = threadIdx.x; n < nf; n += blockDim.x) a.T[warm_col(a, n0 + n)] = a.c_now;
+  }
+}
 
 template <int TK>
 struct KMap {
@@ -600,19 +674,10 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(const SolveArgs a) {
     const int n = idx / KP, k = idx - n * KP;
     float val = 0.0f;
     if (n < nf && k < K) {
-      if (a.h0_mode == 0) {
-        val = a.H0[size_t(n0 + n) * K + k];
-      } else if (a.h0_mode == 1) {
-        const int64_t col = a.widx ? int64_t(a.widx[n0 + n]) : (a.wbase + n0 + n) % a.wmod;
-        const uint32_t tag = a.T[col];
-        const double ratio = a.P[size_t(a.c_now) * K + k] / a.P[size_t(tag) * K + k];
-        val = float(double(a.U[size_t(col) * K + k]) * ratio);
-      } else {
-        const double mv = meanv[n] > a.epsd ? meanv[n] : a.epsd;
-        val = float(mv / a.kst->kmeanw * a.u01[size_t(n0 + n) * K + k]);
-      }
-      if (a.hscale) val = float(double(val) * a.hscale[k]);
-      if (a.check_h0 && !(val > 0.0f)) s_bad = 1;
+      int bad = 0;
+      const int64_t col = a.h0_mode == 1 ? warm_col(a, n0 + n) : 0;
+      val = solve_h0(a, n0 + n, k, col, a.h0_mode == 1 ? a.T[col] : 0u, a.h0_mode == 2 ? meanv[n] : 0.0, bad);
+      if (a.check_h0 && bad) s_bad = 1;
     }
     Hs[idx] = val;
     put_hfrag(Hhi, Hlo, hfrag_index<S::KB>(n, k), val);
@@ -856,19 +921,7 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(const SolveArgs a) {
   }
 
   // final activations
-  if (a.Hout || a.write_store) {
-    for (int idx = tid; idx < NT * KP; idx += kThreads) {
-      const int n = idx / KP, k = idx - n * KP;  // compile-time KP
-      if (n >= nf || k >= K) continue;
-      const float h = Hs[idx];
-      if (a.Hout) a.Hout[size_t(n0 + n) * K + k] = h;
-      if (a.write_store) {
-        const int64_t col = a.widx ? int64_t(a.widx[n0 + n]) : (a.wbase + n0 + n) % a.wmod;
-        a.U[size_t(col) * K + k] = h;
-        if (k == 0) a.T[col] = a.c_now;
-      }
-    }
-  }
+  write_final_h(a, n0, nf, [&](int n, int k) { return Hs[n * KP + k]; });
   PROF_MARK(7);  // epilogue
 }
 
@@ -1322,18 +1375,10 @@ __global__ void __launch_bounds__(kGenThreads, 1) solve_generic_kernel(const Sol
     const int n = idx / KP, k = idx - n * KP;
     float val = 0.0f;
     if (n < nf && k < K) {
-      if (a.h0_mode == 0) {
-        val = a.H0[size_t(n0 + n) * K + k];
-      } else if (a.h0_mode == 1) {
-        const int64_t col = a.widx ? int64_t(a.widx[n0 + n]) : (a.wbase + n0 + n) % a.wmod;
-        const uint32_t tag = a.T[col];
-        val = float(double(a.U[size_t(col) * K + k]) * (a.P[size_t(a.c_now) * K + k] / a.P[size_t(tag) * K + k]));
-      } else {
-        const double mv = meanv[n] > a.epsd ? meanv[n] : a.epsd;
-        val = float(mv / a.kst->kmeanw * a.u01[size_t(n0 + n) * K + k]);
-      }
-      if (a.hscale) val = float(double(val) * a.hscale[k]);
-      if (a.check_h0 && !(val > 0.0f)) s_bad = 1;
+      int bad = 0;
+      const int64_t col = a.h0_mode == 1 ? warm_col(a, n0 + n) : 0;
+      val = solve_h0(a, n0 + n, k, col, a.h0_mode == 1 ? a.T[col] : 0u, a.h0_mode == 2 ? meanv[n] : 0.0, bad);
+      if (a.check_h0 && bad) s_bad = 1;
     }
     Hs[idx] = val;
   }
@@ -1440,18 +1485,7 @@ __global__ void __launch_bounds__(kGenThreads, 1) solve_generic_kernel(const Sol
     }
   }
   __syncthreads();
-  if (a.Hout || a.write_store) {
-    for (int idx = tid; idx < nf * K; idx += kGenThreads) {
-      const int n = idx / K, k = idx - n * K;
-      const float h = Hs[n * KP + k];
-      if (a.Hout) a.Hout[size_t(n0 + n) * K + k] = h;
-      if (a.write_store) {
-        const int64_t col = a.widx ? int64_t(a.widx[n0 + n]) : (a.wbase + n0 + n) % a.wmod;
-        a.U[size_t(col) * K + k] = h;
-        if (k == 0) a.T[col] = a.c_now;
-      }
-    }
-  }
+  write_final_h(a, n0, nf, [&](int n, int k) { return Hs[n * KP + k]; });
 }
 #endif
 

@@ -85,19 +85,10 @@ __global__ void __launch_bounds__(kLgThreads, 1) solve_large_kernel(const SolveA
   }
   for (int idx = tid; idx < nf * K; idx += kLgThreads) {  // h0
     const int n = idx / K, k = idx - n * K;
-    float val;
-    if (a.h0_mode == 0) {
-      val = a.H0[size_t(n0 + n) * K + k];
-    } else if (a.h0_mode == 1) {
-      const int64_t col = a.widx ? int64_t(a.widx[n0 + n]) : (a.wbase + n0 + n) % a.wmod;
-      const uint32_t tag = a.T[col];
-      val = float(double(a.U[size_t(col) * K + k]) * (a.P[size_t(a.c_now) * K + k] / a.P[size_t(tag) * K + k]));
-    } else {
-      const double mv = meanv[n] > a.epsd ? meanv[n] : a.epsd;
-      val = float(mv / a.kst->kmeanw * a.u01[size_t(n0 + n) * K + k]);
-    }
-    if (a.hscale) val = float(double(val) * a.hscale[k]);
-    if (a.check_h0 && !(val > 0.0f)) s_bad = 1;
+    int bad = 0;
+    const int64_t col = a.h0_mode == 1 ? warm_col(a, n0 + n) : 0;
+    const float val = solve_h0(a, n0 + n, k, col, a.h0_mode == 1 ? a.T[col] : 0u, a.h0_mode == 2 ? meanv[n] : 0.0, bad);
+    if (a.check_h0 && bad) s_bad = 1;
     Hs[n * KPS + k] = val;
   }
   __syncthreads();
@@ -349,18 +340,7 @@ __global__ void __launch_bounds__(kLgThreads, 1) solve_large_kernel(const SolveA
       a.divpart[blockIdx.x] = s;
     }
   }
-  if (a.Hout || a.write_store) {
-    for (int idx = tid; idx < nf * K; idx += kLgThreads) {
-      const int n = idx / K, k = idx - n * K;
-      const float h = Hs[n * KPS + k];
-      if (a.Hout) a.Hout[size_t(n0 + n) * K + k] = h;
-      if (a.write_store) {
-        const int64_t col = a.widx ? int64_t(a.widx[n0 + n]) : (a.wbase + n0 + n) % a.wmod;
-        a.U[size_t(col) * K + k] = h;
-        if (k == 0) a.T[col] = a.c_now;
-      }
-    }
-  }
+  write_final_h(a, n0, nf, [&](int n, int k) { return Hs[n * KPS + k]; });
 }
 
 }  // namespace isnmf_dev

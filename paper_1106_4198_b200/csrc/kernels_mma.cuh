@@ -440,7 +440,7 @@ __global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a
     const int64_t fr = tid < nf ? (a.vsel ? a.vsel[n0 + tid] : a.v0 + n0 + tid) : 0;
     fptr[tid] = a.V + fr * a.ldv;
     if (a.h0_mode == 1 && tid < nf) {  // per-frame warm-store column and tag, off the per-element chain
-      const int64_t col = a.widx ? int64_t(a.widx[n0 + tid]) : (a.wbase + n0 + tid) % a.wmod;
+      const int64_t col = warm_col(a, n0 + tid);
       colv[tid] = col;
       tagv[tid] = a.T[col];
     }
@@ -461,18 +461,10 @@ __global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a
     const int n = idx / KP, k = idx - n * KP;
     float val = 0.0f;
     if (n < nf && k < K) {
-      if (a.h0_mode == 0) {
-        val = a.H0[size_t(n0 + n) * K + k];
-      } else if (a.h0_mode == 1) {
-        const int64_t col = colv[n];
-        const double ratio = a.P[size_t(a.c_now) * K + k] / a.P[size_t(tagv[n]) * K + k];
-        val = float(double(a.U[size_t(col) * K + k]) * ratio);
-      } else {
-        const double mv = meanv[n] > a.epsd ? meanv[n] : a.epsd;
-        val = float(mv / a.kst->kmeanw * a.u01[size_t(n0 + n) * K + k]);
-      }
-      if (a.hscale) val = float(double(val) * a.hscale[k]);
-      if (a.check_h0 && !(val > 0.0f)) s_bad = 1;
+      int bad = 0;
+      val = a.h0_mode == 1 ? solve_h0(a, n0 + n, k, colv[n], tagv[n], 0.0, bad)
+                           : solve_h0(a, n0 + n, k, 0, 0u, a.h0_mode == 2 ? meanv[n] : 0.0, bad);
+      if (a.check_h0 && bad) s_bad = 1;
     }
     put_hf(Hf + hf_index<KB>(n, k), val);
   }
@@ -632,19 +624,7 @@ __global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a
   }
 
   // final activations
-  if (a.Hout || a.write_store) {
-    for (int idx = tid; idx < NT * KP; idx += kMmThreads) {
-      const int n = idx / KP, k = idx - n * KP;
-      if (n >= nf || k >= K) continue;
-      const float h = Hf[hf_index<KB>(n, k)];
-      if (a.Hout) a.Hout[size_t(n0 + n) * K + k] = h;
-      if (a.write_store) {
-        const int64_t col = a.widx ? int64_t(a.widx[n0 + n]) : (a.wbase + n0 + n) % a.wmod;
-        a.U[size_t(col) * K + k] = h;
-        if (k == 0) a.T[col] = a.c_now;
-      }
-    }
-  }
+  write_final_h(a, n0, nf, [&](int n, int k) { return Hf[hf_index<KB>(n, k)]; });
   MM_STAMP(63);
 }
 
