@@ -9,8 +9,12 @@
 // before every callback).  online_resume pulls frames from the source in blocks
 // that end on mini-batch boundaries and hands each block to one engine call;
 // without a callback and with eta == 0 it runs up to 64 mini-batches per call.
-// Checkpointing (online.hpp:421-489) is persistence and is not part of this
-// engine.
+// warm_h round-trips exactly: the engine's warm activation store is fp64 like the
+// reference's (values below fp32's range enter the fp32 solver at a floor that
+// leaves W h unchanged and are rescaled back in fp64; kernels.cuh warm_value).
+// Checkpointing (save_checkpoint / load_checkpoint, the reference's "ISCK"
+// format, online.hpp:421-489) serialises these host fields; see the end of
+// this file.
 #pragma once
 
 #include <algorithm>
