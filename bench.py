@@ -58,6 +58,7 @@ def parse(argv=None):
     p.add_argument("--cpu-sample-batches", type=int, default=4)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-compare", action="store_true", help="skip the batch-vs-online comparison")
     return p.parse_args(argv)
 
 
@@ -226,13 +227,32 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def cpu_batch_rate(F, K, n_sample, epochs_sample=1):
+    """Oracle batch_train (fp64 restatement of batch.hpp:84-143) on a sample of
+    n_sample frames: seconds per epoch per frame (the epoch cost is linear in N)."""
+    import oracle as O
+    from tools.synth import spectrogram_np
+    v = spectrogram_np(F, K, n_sample, seed=61).astype(np.float64)
+    rng = np.random.default_rng(62)
+    w0 = rng.uniform(0.1, 1.0, size=(F, K))
+    h0 = rng.uniform(0.1, 1.0, size=(K, n_sample))
+    t0 = time.perf_counter()
+    O.batch_train(v, w0, h0, epochs_sample)
+    dt = time.perf_counter() - t0
+    return dt / (epochs_sample * n_sample), dt
+
+
 def run_batch(args, rank, world):
-    """Config 2: batch IS-NMF, 100 MU epochs over F=513 x N=225k (O(FKN) comparison path)."""
+    """Config 2: batch IS-NMF, 100 MU epochs over F=513 x N=225k (O(FKN) comparison path).
+    value = epochs/s from CUDA events around the enqueued epochs (isnmf_batch_profile);
+    e2e = the same call with V in pinned host memory, host-timed (V and H uploads, W and
+    H downloads included)."""
     import torch
 
     import paper_1106_4198_b200 as E
     from tools.synth import spectrogram_torch
-    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)) % max(torch.cuda.device_count(), 1))
+    dev = int(os.environ.get("LOCAL_RANK", rank)) % max(torch.cuda.device_count(), 1)
+    torch.cuda.set_device(dev)
     cfg = dict(CONFIGS["c2"])
     F, K, N = cfg["F"], cfg["K"], args.frames or cfg["N"]
     epochs = cfg["epochs"]
@@ -241,27 +261,139 @@ def run_batch(args, rank, world):
     w0 = rng.uniform(0.1, 1.0, size=(F, K))
     h0 = rng.uniform(0.1, 1.0, size=(K, N))
     torch.cuda.synchronize()
-    E.batch_train(vd, w0, h0, 2)  # warm-up
-    torch.cuda.synchronize()
-    times = []
-    for _ in range(args.steps):
-        barrier(world)
-        t0 = time.perf_counter()
-        out = E.batch_train(vd, w0, h0, epochs)
-        torch.cuda.synchronize()
-        times.append(allmax(time.perf_counter() - t0, world))
-    t = float(np.median(times))
+    E.batch_profile(1)
+    for _ in range(max(1, args.warmup)):
+        E.batch_train(vd, w0, h0, 2)
+    times, launches = [], 0
+    with ClockSampler(dev) as clk:
+        time.sleep(0.5)
+        for _ in range(args.steps):
+            barrier(world)
+            torch.cuda.synchronize()
+            out = E.batch_train(vd, w0, h0, epochs)
+            ms, nl = E.batch_profile()
+            torch.cuda.synchronize()
+            barrier(world)
+            times.append(allmax(ms, world))
+            launches += nl
+    t = float(np.sum(times)) / 1e3 / args.steps
     flops = 12.0 * F * K * N * epochs + 2.0 * F * K * N
+    peak = FP32_PEAK_NOMINAL
+    e2e = None
+    if not args.no_e2e:
+        vh = torch.empty_like(vd, device="cpu").pin_memory()
+        vh.copy_(vd)
+        E.batch_train(vh, w0, h0, 1)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            E.batch_train(vh, w0, h0, epochs)
+        e2e_s = allmax((time.perf_counter() - t0) / args.steps, world)
+        e2e = {"value": world * epochs / e2e_s, "unit": "epochs/s", "h2d_bytes_per_step": int(N * F * 4 + K * N * 4),
+               "d2h_bytes_per_step": int(K * N * 4 + F * K * 8),
+               "timing": "host wall clock of the whole batch_train call with V in pinned host memory"}
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        n_s = 4000
+        spf, dt = cpu_batch_rate(F, K, n_s)
+        cpu_name, ncpu = host_info()
+        cpu = {"value": 1.0 / (spf * N), "unit": "epochs/s", "cores": 1, "kind": "port",
+               "sample": f"1 epoch over {n_s} frames ({dt:.1f} s) of the c2 shape, scaled to N={N} (the epoch "
+                         f"cost is linear in N); fp64 oracle restatement of batch.hpp:84-143 on 1 core of "
+                         f"{cpu_name} ({ncpu} cores)"}
     if rank == 0:
         print(json.dumps({"metric": "batch IS-NMF epochs/sec (F=513,K=50,N=225k)", "value": world * epochs / t,
-                          "unit": "epochs/s", "n_gpus": world, "steps": args.steps, "warmup": 1,
+                          "unit": "epochs/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                           "ms_per_step": 1e3 * t, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
                           "dtype": "f32", "data": "synthetic",
-                          "config": {"workload": f"c2: F={F}, K={K}, N={N}, {epochs} epochs (host-timed, includes "
-                                                 f"H upload/download)",
-                                     "parallelism": "replicas" if world > 1 else "single"},
-                          "achieved_tflops": flops / t / 1e12, "final_obj": float(out["obj"][-1]),
-                          "initial_obj": out["initial_obj"]}), flush=True)
+                          "config": {"workload": f"c2: F={F}, K={K}, N={N}, {epochs} epochs per step, W0/H0 ~ "
+                                                 f"U(0.1,1); V device-resident, device-timed (CUDA events)",
+                                     "parallelism": "replicas" if world > 1 else "single",
+                                     "l2": "inputs larger than L2 (V = %.2f GB fp32)" % (N * F * 4 / 1e9)},
+                          "roofline": {"bound": "fp32", "achieved": flops / t / 1e12, "peak": peak,
+                                       "unit": "TFLOP/s", "frac": flops / t / 1e12 / peak,
+                                       "flops_per_step": flops,
+                                       "flop_model": "12FKN per epoch (H pass 6FKN + statistics 6FKN; the "
+                                                     "objective shares the next epoch's first W h) + 2FKN",
+                                       "traffic": None,
+                                       "peak_source": "nominal FP32 FMA peak 148 SM x 128 x 2 x 1.965 GHz"},
+                          "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clk.summary(),
+                          "final_obj": float(out["obj"][-1]), "initial_obj": out["initial_obj"]}), flush=True)
+
+
+def objective_device(vd, w, h, eps=1e-12):
+    """(1/N) sum is_term((V - WH) / (eps + WH)) (kernels.hpp:43-55) in fp64 on the device
+    (torch; a measurement aid for the comparison below, not the engine)."""
+    import torch
+    wt = torch.from_numpy(np.ascontiguousarray(w)).cuda()
+    ht = torch.from_numpy(np.ascontiguousarray(h)).cuda()
+    acc, n = 0.0, vd.shape[0]
+    for s0 in range(0, n, 1 << 16):
+        x = wt @ ht[:, s0:s0 + (1 << 16)]
+        u = (vd[s0:s0 + (1 << 16), :w.shape[0]].T.double() - x) / (eps + x)
+        acc += float(torch.clamp(u - torch.log1p(u), min=0.0).sum())
+    return acc / n
+
+
+def batch_vs_online(seed=4040):
+    """north_star: batch-vs-online wall-clock on the same data, next to the host CPU.
+    Data: the config-2 spectrogram (F=513, N=225k, K*=50) on the device.  Online: K=50,
+    config 1's mini-batch beta=1000 and I=10, one pass, rho=1, W0 (l1-normalised
+    U(0.1,1)), A0=B0=1e-3, warm H0=1.  Batch: 100 epochs (config 2) from the same W0 and
+    H0=1.  Device times from CUDA events; objective = the batch objective of (W, H) with
+    H = the online warm store.  CPU: the fp64 oracle on 1 core, projected from samples."""
+    import torch
+
+    import paper_1106_4198_b200 as E
+    from tools.synth import spectrogram_np, spectrogram_torch, w_init
+    F, K, N, beta, iters, epochs = 513, 50, 225_000, 1000, 10, 100
+    vd = spectrogram_torch(F, K, N, seed=seed, shape=0.5, device="cuda")
+    w0 = w_init(F, K, seed + 1)
+    a0 = np.full((F, K), 1e-3)
+    eng = E.Online(F, K, beta, iters, restart="warm", n_store=N)
+    on_ms = []
+    for _ in range(2):  # the first run warms up
+        eng.set_dictionary(w0, a0, a0)
+        eng.set_counters(0, 0, 1.0)
+        eng.fill_warm_h(1.0)
+        torch.cuda.synchronize()
+        prof = E.Profile(eng, per_kernel=False)
+        prof.start()
+        eng.enqueue(vd, N, vd.stride(0))
+        eng.synchronize()
+        on_ms.append(prof.stop()["span_ms"])
+    st = eng.state(warm_h=True)
+    eng.close()
+    on_obj = objective_device(vd, st["w"], st["warm_h"])
+    h0 = np.ones((K, N))
+    E.batch_profile(1)
+    E.batch_train(vd, w0, h0, 2)
+    out = E.batch_train(vd, w0, h0, epochs)
+    b_ms, _ = E.batch_profile()
+    b_obj = np.asarray(out["obj"])
+    hit = np.nonzero(b_obj <= on_obj)[0]
+    ep_match = int(hit[0]) + 1 if hit.size else None
+    del vd
+    torch.cuda.empty_cache()
+    # CPU (fp64 oracle, 1 core): online frames/s on 4 mini-batches, batch s/epoch/frame on 2000 frames
+    import oracle as O
+    vs = spectrogram_np(F, K, 4 * beta, seed=seed + 2)
+    t0 = time.perf_counter()
+    O.baseline_online(vs, w0, a0, a0, beta, iters, 1.0, threads=1)
+    cpu_on_fps = 4 * beta / (time.perf_counter() - t0)
+    spf, _ = cpu_batch_rate(F, K, 2000)
+    cpu_name, _ = host_info()
+    return {"data": f"F={F}, N={N}, K*={K} synthetic (config 2's spectrogram)",
+            "online": {"config": f"K={K}, beta={beta}, I={iters}, 1 pass, rho=1, warm H0=1, A0=B0=1e-3",
+                       "gpu_ms": float(on_ms[-1]), "objective": on_obj,
+                       "cpu_1core_s_projected": N / cpu_on_fps},
+            "batch": {"config": f"K={K}, {epochs} epochs, H0=1", "gpu_ms": float(b_ms),
+                      "objective_after_epochs": float(b_obj[-1]),
+                      "epochs_to_reach_online_objective": ep_match,
+                      "gpu_ms_to_reach_online_objective": (None if ep_match is None
+                                                           else float(b_ms) * ep_match / epochs),
+                      "cpu_1core_s_projected": epochs * N * spf},
+            "cpu": f"fp64 oracle port, 1 core of {cpu_name}; online timed on {4 * beta} frames, batch on "
+                   f"1 epoch of 2000 frames, projected to N={N} (per-frame cost independent of N)"}
 
 
 def run_engine(args, rank, world):
@@ -385,6 +517,9 @@ def run_engine(args, rank, world):
                          f"({ncpu} cores); the reference itself cannot be compiled (no Eigen)"}
 
     traffic, traffic_src = k1_traffic(args.config)
+    compare = None
+    if rank == 0 and args.config == "c3" and not args.no_compare:
+        compare = batch_vs_online()
     if rank == 0:
         metric = ("online IS-NMF frames/sec (F=513,K=50,beta=4096)" if args.config == "c3" else
                   f"online IS-NMF frames/sec ({args.config}: F={F},K={K},beta={beta})")
@@ -418,7 +553,7 @@ def run_engine(args, rank, world):
                              "peak_source": "nominal FP32 FMA peak 148 SM x 128 x 2 x 1.965 GHz = 74.4 TFLOP/s "
                                             "(MEASURED_PEAKS.json has no FP32 entry; tools/probe measured 72.4 "
                                             "on this pool)"},
-                "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches,
+                "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches, "batch_vs_online": compare,
                 "clocks": clk.summary(), "wall_s": wall,
                 "final": {"t": st["t"], "commits": st["commits"], "last_minibatch_obj": st["last_minibatch_obj"]}}
         print(json.dumps(line), flush=True)

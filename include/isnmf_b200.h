@@ -194,6 +194,12 @@ int isnmf_batch_train(const float* v, int64_t ldv, int64_t F, int64_t N, int64_t
                       const double* h0, uint64_t max_epochs, double epsilon, double eta, double* w_out,
                       double* h_out, double* obj_trace, uint64_t* epochs, double* initial_obj, double* last_delta);
 
+/* Profiling (not part of the reference interface): enable >= 0 switches CUDA-event
+ * timing of isnmf_batch_train on (1) or off (0); -1 leaves it.  Returns the device
+ * time of the last timed call (its enqueued epochs and final objective pass, without
+ * the V / H transfers) and how many engine kernels it launched. */
+int isnmf_batch_profile(int32_t enable, double* device_ms, int64_t* launches);
+
 /* ---------------------------------------------------------------------------
  * Held-out fit — evaluate_heldout (harness.hpp:17-37): H from the reference's
  * seed-deterministic uniform stream scaled by max(mean test, eps)/(K mean W),

@@ -76,6 +76,7 @@ _SIGS = {
     "isnmf_online_profile_begin": ([VP, C.c_int32], C.c_int),
     "isnmf_online_profile_end": ([VP, VP, VP, VP, VP, VP], C.c_int),
     "isnmf_batch_train": ([VP, I64, I64, I64, I64, VP, VP, U64, D, D, VP, VP, VP, VP, VP, VP], C.c_int),
+    "isnmf_batch_profile": ([I32, VP, VP], C.c_int),
     "isnmf_evaluate_heldout": ([VP, I64, I64, I64, VP, I64, D, C.c_int32, U64, VP], C.c_int),
     "isnmf_stft_power": ([VP, I64, C.c_int32, C.c_int32, VP, I64, VP], C.c_int),
     "isnmf_discard_silence": ([VP, I64, I64, D, VP, VP], C.c_int),
@@ -319,6 +320,14 @@ def batch_train(v32, w0, h0, max_epochs, eps=1e-12, eta=0.0):
     _check(lib().isnmf_batch_train(_p(v32), ldv, F, N, K, _p(w0), _p(h0), max_epochs, eps, eta, _p(w), _p(h),
                                    _p(obj), C.byref(ep), C.byref(o0), C.byref(ld)))
     return dict(w=w, h=h, obj=obj[:ep.value].copy(), epochs=ep.value, initial_obj=o0.value, last_delta=ld.value)
+
+
+def batch_profile(enable=-1):
+    """CUDA-event device time (ms) and kernel launches of the last batch_train call
+    (enable=1/0 switches the timing on/off first)."""
+    ms, n = D(), I64()
+    _check(lib().isnmf_batch_profile(enable, C.byref(ms), C.byref(n)))
+    return ms.value, n.value
 
 
 def evaluate_heldout(test32, w, eps=1e-12, inner_iters=100, seed=0x45):

@@ -275,6 +275,7 @@ int mma_min_frames() {
 }
 
 struct SolvePlan {
+  bool tiled = false;       // the kernel loops over frame tiles (K1M): any grid <= tiles works
   LargeFn large = nullptr;  // tensor-pipe kernels (large K, or the resident-dictionary variant)
   int threads = 0;          // block size of `large`
   Variant* var = nullptr;  // nullptr: generic
@@ -303,6 +304,7 @@ int plan_solve(int64_t F, int64_t K, int64_t frames, SolvePlan* plan, bool force
         mma_configured[wi][fg - 1][kb - 1] = true;
       }
       plan->large = mma_kernel(nw, fg, kb);
+      plan->tiled = true;
       plan->threads = 32 * nw;
       plan->var = nullptr;
       plan->NT = nt;
@@ -1302,6 +1304,14 @@ __global__ void sum_partials(const double* part, int n, double* out) {
   }
 }
 
+struct BatchProfile {
+  bool on = false;
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  double device_ms = 0.0;
+  int64_t launches = 0;
+};
+BatchProfile g_prof;
+
 // A device workspace for the fused solve over an arbitrary set of frames.
 struct SolveWork {
   int F = 0, K = 0, WS = 0, KP = 0, NT = 0;
@@ -1316,10 +1326,13 @@ struct SolveWork {
   float* stats = nullptr;
   double* divpart = nullptr;
   unsigned int* halt = nullptr;
+  double* obj_trace = nullptr;  // batch: objective of (W_{e-1}, H_{e-1}) recorded by epoch e's commit
+  long long obj_cap = 0;
+  int64_t launches = 0;
 
   ~SolveWork() {
     if (s) cudaStreamSynchronize(s);
-    void* ptrs[] = {st, W32, W64, pa, pb, A, B, cta_part, P, scale, stats, divpart, halt};
+    void* ptrs[] = {st, W32, W64, pa, pb, A, B, cta_part, P, scale, stats, divpart, halt, obj_trace};
     for (void* p : ptrs) dfree(p);
     if (s) cudaStreamDestroy(s);
   }
@@ -1370,12 +1383,19 @@ struct SolveWork {
 
   // One fused pass over frames [0, n) of V (device, ld ldv): h0 from H (device
   // [n][K]) scaled by hscale, `iters` MM iterations, H written back in place;
-  // statistics reduced into pa/pb and the divergence into st->pending_div.
+  // statistics reduced into pa/pb and the divergence into st->pending_div.  With
+  // `commit` the last fold also commits (batch: rho = 0, column scales -> scale,
+  // epoch bookkeeping on the device, eta stop through the halt flag).
+  // K1M (tiled) covers all n frames in one launch of one CTA per SM; the other
+  // kernels run segments of seg_blocks CTAs, each followed by a fold.
   int pass(const float* V, int64_t ldv, int64_t n, float* H, int iters, double eps, const double* hscale,
-           bool stats_on, bool div_first, bool check_h0) {
-    for (int64_t s0 = 0; s0 < n; s0 += int64_t(seg_blocks) * NT) {
-      const int64_t ns = std::min<int64_t>(n - s0, int64_t(seg_blocks) * NT);
-      const int nblk = int((ns + NT - 1) / NT);
+           bool stats_on, bool div_first, bool check_h0, bool commit = false, double eta = 0.0,
+           const unsigned int* halt_in = nullptr) {
+    const int64_t seg = plan.tiled ? std::max<int64_t>(n, 1) : int64_t(seg_blocks) * NT;
+    for (int64_t s0 = 0; s0 < n; s0 += seg) {
+      const int64_t ns = std::min<int64_t>(n - s0, seg);
+      const int64_t tiles = (ns + NT - 1) / NT;
+      const int nblk = int(plan.tiled ? std::min<int64_t>(tiles, device_sms()) : tiles);
       SolveArgs a{};
       a.W32 = W32;
       a.F = F;
@@ -1397,14 +1417,27 @@ struct SolveWork {
       a.stats = stats_on ? stats : nullptr;
       a.divpart = divpart;
       a.status = &st->status;
-      a.halt = halt;
-      launch_solve(plan, nblk, a, s);
+      a.halt = halt_in ? halt_in : halt;
+      if (nblk > 0) {
+        launch_solve(plan, nblk, a, s);
+        launches++;
+      }
       FoldArgs r = fold_args();
+      r.halt = halt_in ? const_cast<unsigned int*>(halt_in) : halt;
       r.nstat = stats_on ? nblk : 0;
       r.ndiv = nblk;
       r.nframes = int(ns);
-      r.do_commit = 0;
+      r.do_commit = commit && s0 + seg >= n;
+      if (r.do_commit) {
+        r.rho = 0.0;
+        r.scale_out = scale;
+        r.batch_mode = 1;
+        r.eta = eta;
+        r.tr_obj = obj_trace;
+        r.tr_cap = obj_cap;
+      }
       TRY(launch_fold(r, s));
+      launches++;
       CU(cudaGetLastError());
     }
     return 0;
@@ -1616,7 +1649,7 @@ int isnmf_batch_train(const float* v, int64_t ldv, int64_t F, int64_t N, int64_t
   SolveWork wk;
   TRY(wk.init(F, K, N));
   TRY(wk.set_w(w0));
-  DevBuf bv, bh, bs;
+  DevBuf bv, bh;
   const float* dv = v;
   int64_t dld = ldv;
   if (!is_device_ptr(v)) {
@@ -1631,80 +1664,54 @@ int isnmf_batch_train(const float* v, int64_t ldv, int64_t F, int64_t N, int64_t
   float* dh = nullptr;
   TRY(upload_h(h0, K, N, &dh));
   bh.p = dh;
-  double* dscale = nullptr;  // rescale factors to apply on the next H read
-  TRY(dalloc(&dscale, size_t(K)));
-  bs.p = dscale;
-  fill_f64<<<1, 256, 0, wk.s>>>(dscale, K, 1.0);
+  // the column scales of the last commit multiply H on its next read (rescale_dictionary's
+  // H compensation, model.hpp:84, applied lazily)
+  fill_f64<<<1, 256, 0, wk.s>>>(wk.scale, K, 1.0);
   fill_f64<<<1, 256, 0, wk.s>>>(wk.P, 2 * K, 1.0);
-  const double dK = double(K);
-  (void)dK;
-  double prev = 0.0;
-  uint64_t done = 0;
-  double delta = 0.0;
-  for (uint64_t e = 1; e <= max_epochs; ++e) {
-    // reset per-epoch accumulators
-    CU(cudaMemsetAsync(wk.pa, 0, size_t(F) * K * sizeof(double), wk.s));
-    CU(cudaMemsetAsync(wk.pb, 0, size_t(F) * K * sizeof(double), wk.s));
-    {
-      DevState h{};
-      TRY(wk.state(&h));
-      if (h.status) return status_to_code(h.status, "batch_train", 0);
-      h.pending_div = 0.0;
-      h.pending_count = 0;
-      CU(cudaMemcpy(wk.st, &h, sizeof(h), cudaMemcpyHostToDevice));
+  wk.obj_cap = (long long)max_epochs + 1;
+  TRY(dalloc(&wk.obj_trace, size_t(wk.obj_cap)));
+  if (g_prof.on) CU(cudaEventRecord(g_prof.ev[0], wk.s));
+  // Every epoch is enqueued without a host round trip (batch.hpp:104-141): K1 runs one MM
+  // iteration over all N frames with the objective of the incoming (W_{e-1}, H_{e-1})
+  // from its first Lam and the statistics of the updated H; K2 folds them and commits
+  // with rho = 0 (A, B = the statistics, W = sqrt(A/B), l1 rescale).  K2's last CTA
+  // records the objective, raises DivergedObjective (batch.hpp:129-131) and sets the
+  // halt flag on ||dW||_F < eta, after which every queued kernel returns at once.
+  for (uint64_t e = 1; e <= max_epochs; ++e)
+    TRY(wk.pass(dv, dld, N, dh, 1, eps, wk.scale, true, true, false, true, eta));
+  DevState h{};
+  TRY(wk.state(&h));
+  const uint64_t done = h.commits;
+  std::vector<double> tr(size_t(wk.obj_cap));
+  CU(cudaMemcpy(tr.data(), wk.obj_trace, tr.size() * sizeof(double), cudaMemcpyDeviceToHost));
+  if (h.status & ST_DIVERGED)
+    return fail(ISNMF_E_DIVERGED_OBJECTIVE, "batch_train: objective increased at epoch %llu",
+                (unsigned long long)done);
+  if (h.status) return status_to_code(h.status, "batch_train", done);
+  const double delta = h.last_delta;
+  // final objective of (W_e, H_e): a divergence-only pass that also applies the last
+  // rescale to H (the halt flag is cleared so it runs after an eta stop)
+  h.pending_div = 0.0;
+  h.pending_count = 0;
+  CU(cudaMemcpy(wk.st, &h, sizeof(h), cudaMemcpyHostToDevice));
+  CU(cudaMemset(wk.halt, 0, sizeof(unsigned int)));
+  TRY(wk.pass(dv, dld, N, dh, 0, eps, wk.scale, false, false, false));
+  if (g_prof.on) CU(cudaEventRecord(g_prof.ev[1], wk.s));
+  TRY(wk.state(&h));
+  if (h.status) return status_to_code(h.status, "batch_train", done);
+  const double obj = h.pending_div / double(N);
+  if (done >= 1) {
+    const double prev = tr[done - 1];
+    if (obj > prev + 1e-6 * prev + 1e-15)
+      return fail(ISNMF_E_DIVERGED_OBJECTIVE, "batch_train: objective increased at epoch %llu",
+                  (unsigned long long)done);
+    if (initial_obj) *initial_obj = tr[0];
+    if (obj_trace) {
+      for (uint64_t i = 0; i + 1 < done; ++i) obj_trace[i] = tr[i + 1];
+      obj_trace[done - 1] = obj;
     }
-    TRY(wk.pass(dv, dld, N, dh, 1, eps, dscale, true, true, false));
-    // commit with rho = 0: A = stats, B = stats, W = sqrt(A/B), l1 rescale (scales -> dscale for H);
-    // P indexed by st->commits: commits stays 0 (2-row P)
-    FoldArgs r = wk.fold_args();
-    r.nstat = 0;
-    r.ndiv = 0;
-    r.nframes = 0;
-    r.do_commit = 1;
-    r.rho = 0.0;
-    r.scale_out = dscale;
-    r.batch_mode = 1;
-    TRY(launch_fold(r, wk.s));
-    CU(cudaGetLastError());
-    DevState h{};
-    TRY(wk.state(&h));
-    if (h.status) return status_to_code(h.status, "batch_train", e);
-    const double obj_prev = h.last_obj;  // objective of (W_{e-1}, H_{e-1})
-    if (e == 1) {
-      prev = obj_prev;
-      if (initial_obj) *initial_obj = obj_prev;
-    } else {
-      if (obj_prev > prev + 1e-6 * prev + 1e-15)
-        return fail(ISNMF_E_DIVERGED_OBJECTIVE, "batch_train: objective increased at epoch %llu",
-                    (unsigned long long)(e - 1));
-      prev = obj_prev;
-      if (obj_trace) obj_trace[e - 2] = obj_prev;
-    }
-    h.commits = 0;  // P stays 2 rows
-    CU(cudaMemcpy(wk.st, &h, sizeof(h), cudaMemcpyHostToDevice));
-    delta = h.last_delta;
-    done = e;
-    if (delta < eta) break;
-  }
-  // final objective of (W_e, H_e): divergence-only pass that also applies the last rescale to H
-  {
-    DevState h{};
-    TRY(wk.state(&h));
-    h.pending_div = 0.0;
-    h.pending_count = 0;
-    CU(cudaMemcpy(wk.st, &h, sizeof(h), cudaMemcpyHostToDevice));
-    TRY(wk.pass(dv, dld, N, dh, 0, eps, dscale, false, false, false));
-    TRY(wk.state(&h));
-    if (h.status) return status_to_code(h.status, "batch_train", done);
-    const double obj = h.pending_div / double(N);
-    if (done >= 1) {
-      if (obj > prev + 1e-6 * prev + 1e-15)
-        return fail(ISNMF_E_DIVERGED_OBJECTIVE, "batch_train: objective increased at epoch %llu",
-                    (unsigned long long)done);
-      if (obj_trace) obj_trace[done - 1] = obj;
-    } else if (initial_obj) {
-      *initial_obj = obj;
-    }
+  } else if (initial_obj) {
+    *initial_obj = obj;
   }
   CU(cudaMemcpy(w_out, wk.W64, size_t(F) * K * sizeof(double), cudaMemcpyDeviceToHost));
   std::vector<float> h32(size_t(K) * N);
@@ -1712,6 +1719,28 @@ int isnmf_batch_train(const float* v, int64_t ldv, int64_t F, int64_t N, int64_t
   for (size_t i = 0; i < h32.size(); ++i) h_out[i] = h32[i];
   if (epochs) *epochs = done;
   if (last_delta) *last_delta = delta;
+  if (g_prof.on) {
+    float ms = 0.0f;
+    CU(cudaEventElapsedTime(&ms, g_prof.ev[0], g_prof.ev[1]));
+    g_prof.device_ms = ms;
+    g_prof.launches = wk.launches;
+  }
+  return 0;
+}
+
+// Device time of the last isnmf_batch_train call (CUDA events on its stream
+// around the enqueued epochs and the final objective pass, i.e. without the
+// V / H uploads and downloads) and the kernels it launched; profiling only.
+int isnmf_batch_profile(int32_t enable, double* device_ms, int64_t* launches) {
+  if (enable >= 0) {
+    if (!g_prof.ev[0]) {
+      CU(cudaEventCreate(&g_prof.ev[0]));
+      CU(cudaEventCreate(&g_prof.ev[1]));
+    }
+    g_prof.on = enable != 0;
+  }
+  if (device_ms) *device_ms = g_prof.device_ms;
+  if (launches) *launches = g_prof.launches;
   return 0;
 }
 

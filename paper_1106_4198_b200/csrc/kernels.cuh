@@ -1215,7 +1215,7 @@ __global__ void __cluster_dims__(kFoldCluster, 1, 1) __launch_bounds__(kFoldThre
   }
   if (ok && r == 0 && tid == 0) {
     const unsigned long long c = a.st->commits;
-    a.P[size_t(c + 1) * a.K + k] = a.P[size_t(c) * a.K + k] * sc;
+    if (!a.batch_mode) a.P[size_t(c + 1) * a.K + k] = a.P[size_t(c) * a.K + k] * sc;
     if (a.scale_out) a.scale_out[k] = sc;
   }
   if (!ok && tid == 0) atomicOr(&a.st->pad, ST_ZERO_COLUMN);
@@ -1252,6 +1252,23 @@ __global__ void __cluster_dims__(kFoldCluster, 1, 1) __launch_bounds__(kFoldThre
       return;
     }
     const double delta = sqrt(pd), obj = pc ? pdiv / double(pc) : 0.0;
+    if (a.batch_mode) {
+      // epoch e = c + 1 of batch_train (batch.hpp:104-141): obj is the objective of
+      // (W_{e-1}, H_{e-1}) from this epoch's K1; it must not exceed the previous one
+      // (DivergedObjective, batch.hpp:129-131; the epoch count stays at e - 1)
+      if (c > 0 && obj > st->prev_obj + 1e-6 * st->prev_obj + 1e-15) {
+        st->status |= ST_DIVERGED;
+        return;
+      }
+      st->prev_obj = obj;
+      if (a.tr_obj && (long long)c < a.tr_cap) a.tr_obj[c] = obj;
+      st->last_delta = delta;
+      st->pending_div = 0.0;
+      st->pending_count = 0;
+      st->commits = c + 1;
+      if (a.eta > 0.0 && delta < a.eta) *a.halt = 1u;  // stop after this epoch
+      return;
+    }
     st->last_delta = delta;
     st->kmeanw = double(a.K) * (pw / (double(a.F) * double(a.K)));
     st->last_obj = obj;

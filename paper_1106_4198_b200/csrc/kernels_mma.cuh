@@ -130,6 +130,9 @@ __device__ __forceinline__ void put_hf(float* p, float h) {
 }
 
 __device__ __forceinline__ float2 lds64(const float* p) { return *reinterpret_cast<const float2*>(p); }
+__device__ __forceinline__ void red_add(float* p, float v) {
+  asm volatile("red.relaxed.gpu.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
 
 // One chunk of NBK 8-row blocks (rows row0 ...) of an iteration pass: phase A,
 // q/r in registers, phase B into nd[0] (num^T) / nd[1] (den^T).
@@ -267,7 +270,8 @@ template <int KB, int FG, int WS, int HT>
 __device__ __forceinline__ void mm_stats_block(const float* Ws, const float* Hf, const float* Ht,
                                                const float* const* fptr, int f0, int F, int nf, float eps, int g,
                                                int t, bool want_div, float& divacc, float* outA, float* outB, int FP,
-                                               float (&vv)[2 * FG][4], int f0n, long long* prof, int ev) {
+                                               float (&vv)[2 * FG][4], int f0n, long long* prof, int ev,
+                                               bool accumulate) {
   constexpr int NB = 2 * FG;  // frame blocks of 8
   MM_STAMP_P(prof, ev);
   float acc[NB][4];
@@ -371,19 +375,44 @@ __device__ __forceinline__ void mm_stats_block(const float* Ws, const float* Hf,
   float* pb = outB + size_t(2 * t) * FP + f0 + g;
   const bool ok0 = f0 + g < F, ok1 = f0 + g + 8 < F;
 #pragma unroll
+  if (!accumulate) {
+#pragma unroll
+    for (int j = 0; j < KB; ++j) {
+      const size_t o = size_t(8 * j) * FP;
+      if (ok0) {
+        pa[o] = sa[j][0];
+        pa[o + FP] = sa[j][1];
+        pb[o] = sb[j][0];
+        pb[o + FP] = sb[j][1];
+      }
+      if (ok1) {
+        pa[o + 8] = sa[j][2];
+        pa[o + FP + 8] = sa[j][3];
+        pb[o + 8] = sb[j][2];
+        pb[o + FP + 8] = sb[j][3];
+      }
+    }
+    return;
+  }
+  // A CTA that owns several frame tiles (batch) adds into its planes after the first
+  // with fire-and-forget reductions (red.global.add: no load round trip on the
+  // critical path).  The planes are private to the CTA and every cell has one writer
+  // thread, whose same-address operations are ordered (per-location coherence), so the
+  // sums are formed in tile order: deterministic, bitwise reproducible.
+#pragma unroll
   for (int j = 0; j < KB; ++j) {
     const size_t o = size_t(8 * j) * FP;
     if (ok0) {
-      pa[o] = sa[j][0];
-      pa[o + FP] = sa[j][1];
-      pb[o] = sb[j][0];
-      pb[o + FP] = sb[j][1];
+      red_add(pa + o, sa[j][0]);
+      red_add(pa + o + FP, sa[j][1]);
+      red_add(pb + o, sb[j][0]);
+      red_add(pb + o + FP, sb[j][1]);
     }
     if (ok1) {
-      pa[o + 8] = sa[j][2];
-      pa[o + FP + 8] = sa[j][3];
-      pb[o + 8] = sb[j][2];
-      pb[o + FP + 8] = sb[j][3];
+      red_add(pa + o + 8, sa[j][2]);
+      red_add(pa + o + FP + 8, sa[j][3]);
+      red_add(pb + o + 8, sb[j][2]);
+      red_add(pb + o + FP + 8, sb[j][3]);
     }
   }
 }
@@ -416,8 +445,10 @@ __global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
   const int ntc = a.cta_frames;
-  const int n0 = blockIdx.x * ntc;
-  const int nf = min(ntc, a.nframes - n0);
+  // frame tiles of ntc frames; CTA b owns tiles b, b + gridDim.x, ... (one tile per CTA
+  // for an online mini-batch; the batch path runs one CTA per SM over all N frames, so
+  // the dictionary is loaded once per CTA and the statistics planes accumulate in place)
+  const int ntiles = (a.nframes + ntc - 1) / ntc;
 
   if (tid == 0) {  // dictionary -> smem by TMA bulk copies, overlapped with the h0 set-up below
     const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&wbar));
@@ -436,6 +467,12 @@ __global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a
     }
   }
   for (int i = tid; i < (F16 - F) * WS; i += kMmThreads) Ws[F * WS + i] = 0.0f;  // pad rows
+  double divd = 0.0;  // this lane's divergence over the CTA's tiles
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  const bool first_tile = tile == int(blockIdx.x);
+  const int n0 = tile * ntc;
+  const int nf = min(ntc, a.nframes - n0);
+  if (!first_tile) __syncthreads();  // the previous tile's readers of fptr / Hf / Ht are done
   if (tid < NT) {
     const int64_t fr = tid < nf ? (a.vsel ? a.vsel[n0 + tid] : a.v0 + n0 + tid) : 0;
     fptr[tid] = a.V + fr * a.ldv;
@@ -468,7 +505,7 @@ __global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a
     }
     put_hf(Hf + hf_index<KB>(n, k), val);
   }
-  {  // wait for the dictionary (phase 0 of wbar)
+  if (first_tile) {  // wait for the dictionary (phase 0 of wbar)
     const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&wbar));
     uint32_t done = 0;
     while (!done)
@@ -511,20 +548,25 @@ __global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a
       for (int j = 0; j < KB; ++j)
 #pragma unroll
         for (int c = 0; c < 4; ++c) nd[x][j][c] = 0.0f;
-    int cb = blk0;
-    if (a.div_first && pass == 0) {  // batch: the objective of the incoming (W, H) from this pass
+    // chunks of 4 blocks (4 independent phase-A chains); DIV: the batch objective of the
+    // incoming (W, H) from this pass's Lam (div_first, pass 0)
+    auto chunks = [&](auto div) {
+      constexpr bool DIV = decltype(div)::value;
+      int cb = blk0;
 #pragma unroll 1
-      for (; cb < blk1; ++cb) mm_chunk<KB, WS, 1, true>(Ws, pA, pB, okA, okB, 8 * cb, F, eps, hf, nd, g, t, divacc);
-    }
-#pragma unroll 1
-    for (; cb + 4 <= blk1; cb += 4)
-      mm_chunk<KB, WS, 4, false>(Ws, pA, pB, okA, okB, 8 * cb, F, eps, hf, nd, g, t, divacc);
-    switch (blk1 - cb) {
-      case 3: mm_chunk<KB, WS, 3, false>(Ws, pA, pB, okA, okB, 8 * cb, F, eps, hf, nd, g, t, divacc); break;
-      case 2: mm_chunk<KB, WS, 2, false>(Ws, pA, pB, okA, okB, 8 * cb, F, eps, hf, nd, g, t, divacc); break;
-      case 1: mm_chunk<KB, WS, 1, false>(Ws, pA, pB, okA, okB, 8 * cb, F, eps, hf, nd, g, t, divacc); break;
-      default: break;
-    }
+      for (; cb + 4 <= blk1; cb += 4)
+        mm_chunk<KB, WS, 4, DIV>(Ws, pA, pB, okA, okB, 8 * cb, F, eps, hf, nd, g, t, divacc);
+      switch (blk1 - cb) {
+        case 3: mm_chunk<KB, WS, 3, DIV>(Ws, pA, pB, okA, okB, 8 * cb, F, eps, hf, nd, g, t, divacc); break;
+        case 2: mm_chunk<KB, WS, 2, DIV>(Ws, pA, pB, okA, okB, 8 * cb, F, eps, hf, nd, g, t, divacc); break;
+        case 1: mm_chunk<KB, WS, 1, DIV>(Ws, pA, pB, okA, okB, 8 * cb, F, eps, hf, nd, g, t, divacc); break;
+        default: break;
+      }
+    };
+    if (a.div_first && pass == 0)
+      chunks(std::true_type{});
+    else
+      chunks(std::false_type{});
     MM_STAMP(1 + 4 * pass);
     {  // partials -> shared memory as [warp][num|den][jb][lane][4] (16-byte lane records)
       float* rw = RED + warp * NREG * 32 + lane * 4;
@@ -606,14 +648,18 @@ __global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a
       const int mn = m + kMmThreads / 32;
       mm_stats_block<KB, FG, WS, HT>(Ws, Hf, Ht, fptr, 16 * m, F, nf, eps, g, t, want_div, divacc, outA, outB,
                                          FP, vv, mn < F16 / 16 ? 16 * mn : -1, a.prof,
-                                         44 + 4 * ((m - warp) / (kMmThreads / 32)));
+                                         44 + 4 * ((m - warp) / (kMmThreads / 32)), !first_tile);
     }
   }
+  divd += double(divacc);
+
+  write_final_h(a, n0, nf, [&](int n, int k) { return Hf[hf_index<KB>(n, k)]; });
+  }  // tiles
 
   MM_STAMP(61);
   // divergence partial of this CTA (fixed-order reduction)
   if (a.divpart) {
-    const double d = warp_sum_d(double(divacc));
+    const double d = warp_sum_d(divd);
     if (lane == 0) red[warp] = d;
     __syncthreads();
     if (tid == 0) {
@@ -623,8 +669,6 @@ __global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a
     }
   }
 
-  // final activations
-  write_final_h(a, n0, nf, [&](int n, int k) { return Hf[hf_index<KB>(n, k)]; });
   MM_STAMP(63);
 }
 
