@@ -182,6 +182,14 @@ __device__ __forceinline__ double warm_value(const SolveArgs& a, int64_t col, ui
   return a.U[size_t(col) * a.K + k] * (a.P[size_t(a.c_now) * a.K + k] / a.P[size_t(tag) * a.K + k]);
 }
 
+// a direct or fresh h0 times the optional per-atom scale (batch: the last commit's
+// column scales); flags h0 <= 0 (NonPositiveInit)
+__device__ __forceinline__ float scaled_h0(const SolveArgs& a, float val, int k, int& bad) {
+  if (a.hscale) val = float(double(val) * a.hscale[k]);
+  if (!(val > 0.0f)) bad = 1;
+  return val;
+}
+
 // h0 of launch-local frame n, atom k (n < nframes, k < K) as the solver's fp32
 // start value; sets bad when the reference's solve_h would raise NonPositiveInit
 // (h0 <= 0 or NaN, kernels.hpp:67).  meanv = the frame's mean (fresh mode only).
@@ -199,8 +207,7 @@ __device__ __forceinline__ float solve_h0(const SolveArgs& a, int n, int k, int6
       const double mv = meanv > a.epsd ? meanv : a.epsd;
       val = float(mv / a.kst->kmeanw * a.u01[size_t(n) * a.K + k]);
     }
-    if (a.hscale) val = float(double(val) * a.hscale[k]);
-    if (!(val > 0.0f)) bad = 1;
+    val = scaled_h0(a, val, k, bad);
   }
   return val;
 }
@@ -1025,6 +1032,10 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
+}
 
 // fixed-order block sum (warp tree, then warps in order); valid in thread 0
 __device__ __forceinline__ double block_sum_d(double v, double* red) {

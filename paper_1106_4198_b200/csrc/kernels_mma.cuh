@@ -89,8 +89,10 @@ __device__ __forceinline__ int mm_rho(int n) { return n ^ (n >> 2); }
 
 // is_term (kernels.hpp:15-18) of ratio = (v+eps)/Lam as u - log(ratio) with the
 // fast log: absolute error ~1e-7 per cell (the series of is_term_ratio only
-// buys relative accuracy on terms that are themselves ~1e-7); used for the
-// online objective of the statistics pass
+// buys relative accuracy on terms that are themselves ~1e-7; ~2e-7 relative on a
+// 513-cell frame sum, deterministic); used for the online objective of the
+// statistics pass and for the batch objective of the incoming (W, H) (div_first),
+// whose DivergedObjective guard has 1e-6 relative slack
 __device__ __forceinline__ float is_term_fast(float ratio) {
   const float t = (ratio - 1.0f) - __logf(ratio);
   return t > 0.0f ? t : 0.0f;
@@ -198,7 +200,7 @@ __device__ __forceinline__ void mm_chunk(const float* Ws, const float* pA, const
       const float ve = vv[i][c] + eps;
       q[i][c] = valid ? ve * rr * rr : 0.0f;
       r[i][c] = valid ? rr : 0.0f;
-      if constexpr (DIV) divacc += valid ? is_term_ratio(ve * rr) : 0.0f;
+      if constexpr (DIV) divacc += valid ? is_term_fast(ve * rr) : 0.0f;
     }
   // ---- phase B: per block, K = its 8 rows (slot t <-> c0/c2, slot t+4 <-> c1/c3);
   // the dictionary values of block i+1 are loaded while block i's MMAs issue
@@ -468,11 +470,20 @@ __global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a
   }
   for (int i = tid; i < (F16 - F) * WS; i += kMmThreads) Ws[F * WS + i] = 0.0f;  // pad rows
   double divd = 0.0;  // this lane's divergence over the CTA's tiles
+  // multi-tile CTAs with direct h0 (batch): the next tile's H0 rows are staged into
+  // shared memory by cp.async and its frames prefetched into L2 during this tile's
+  // statistics pass (RED beyond Ht is free then)
+  const bool stage_next = a.h0_mode == 0 && !a.vsel && int(gridDim.x) < ntiles;
+  float* Hstage = RED + ((KP * HT + 31) & ~31);
+  bool staged = false;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
   const bool first_tile = tile == int(blockIdx.x);
   const int n0 = tile * ntc;
   const int nf = min(ntc, a.nframes - n0);
-  if (!first_tile) __syncthreads();  // the previous tile's readers of fptr / Hf / Ht are done
+  if (!first_tile) {
+    if (staged) cp_async_wait_all();
+    __syncthreads();  // the previous tile's readers of fptr / Hf / Ht are done, the staged H0 landed
+  }
   if (tid < NT) {
     const int64_t fr = tid < nf ? (a.vsel ? a.vsel[n0 + tid] : a.v0 + n0 + tid) : 0;
     fptr[tid] = a.V + fr * a.ldv;
@@ -500,6 +511,7 @@ __global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a
     if (n < nf && k < K) {
       int bad = 0;
       val = a.h0_mode == 1 ? solve_h0(a, n0 + n, k, colv[n], tagv[n], 0.0, bad)
+            : staged       ? scaled_h0(a, Hstage[n * K + k], k, bad)
                            : solve_h0(a, n0 + n, k, 0, 0u, a.h0_mode == 2 ? meanv[n] : 0.0, bad);
       if (a.check_h0 && bad) s_bad = 1;
     }
@@ -636,6 +648,18 @@ __global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a
     for (int idx = tid; idx < KP * NT; idx += kMmThreads) {
       const int k = idx / NT, n = idx - k * NT;
       Ht[k * HT + n] = Hf[hf_index<KB>(n, k)];
+    }
+    staged = false;
+    if (stage_next && tile + int(gridDim.x) < ntiles) {
+      const int n1 = (tile + int(gridDim.x)) * ntc, nf1 = min(ntc, a.nframes - n1);
+      const float* src = a.H0 + size_t(n1) * K;
+      for (int i = tid; i < nf1 * K; i += kMmThreads) cp_async4(Hstage + i, src + i);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      const char* v1 = reinterpret_cast<const char*>(a.V + (a.v0 + n1) * a.ldv);
+      const size_t vbytes = size_t(nf1) * a.ldv * sizeof(float);
+      for (size_t off = size_t(tid) * 128; off < vbytes; off += size_t(kMmThreads) * 128)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(v1 + off));
+      staged = true;
     }
     __syncthreads();
     const int FP = (F + 3) & ~3;
