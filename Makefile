@@ -27,6 +27,17 @@ clean:
 	rm -rf $(PKG)/lib $(PKG)/lib_prof oracle/_build oracle/_ref
 .PHONY: all oracle clean
 
+# debug build: device-side index checks (ISNMF_DASSERT, kernels.cuh) that print and trap;
+# select it with ISNMF_LIB=paper_1106_4198_b200/lib_debug/libisnmf_b200.so
+DBG := $(PKG)/lib_debug
+debug: $(DBG)/libisnmf_b200.so
+$(DBG)/libisnmf_b200.so: $(OBJ:$(PKG)/lib/%.o=$(DBG)/%.o)
+	$(NVCC) $(ARCH) -shared -o $@ $^ -lcudart
+$(DBG)/%.o: $(PKG)/csrc/%.cu $(DEPS)
+	@mkdir -p $(DBG)
+	$(NVCC) $(NVFLAGS) -DISNMF_DEBUG -c -o $@ $< 2> $(DBG)/$*.ptxas.log || (cat $(DBG)/$*.ptxas.log; exit 1)
+.PHONY: debug
+
 # experimental build with per-phase cycle counters (K1 headline variant only)
 prof: $(SRC) $(TABLES) $(DEPS)
 	@mkdir -p $(PKG)/lib_prof

@@ -538,7 +538,8 @@ def run_engine(args, rank, world):
                              "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                              "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                              "traffic_unit": "bytes per launch (ncu dram__bytes_read+write)",
-                             "algorithmic_bytes_per_launch": frames_per_launch * (4 * F + 8 * K),
+                             "algorithmic_bytes_per_launch": frames_per_launch * (4 * F + 16 * K),
+                             "algorithmic_bytes_note": "per frame: V read once (4F) + the fp64 warm activation read and written (16K)",
                              "kernel": ("solve_mma_kernel (K1M: 3xTF32 mma.sync for every contraction)"
                                         if K <= 56 and os.environ.get("ISNMF_MMA", "1") != "0" else
                                         "solve_kernel (FP32 FMA + 3xTF32 mma.sync phase A)" if K <= 64 else

@@ -15,7 +15,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libisnmf_b200.so")
+# ISNMF_LIB selects another build of the same library (the debug build, make debug)
+LIB_PATH = os.environ.get("ISNMF_LIB") or os.path.join(_HERE, "lib", "libisnmf_b200.so")
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "isnmf_b200.h")
 
 ERRORS = {

@@ -610,6 +610,8 @@ FoldArgs fold_args(const isnmf_online* c) {
   r.tr_ns = c->tr_ns;
   r.tr_cap = c->tr_cap;
   r.tprof = c->fold_prof;
+  r.stats_cap = c->maxblk;
+  r.p_cap = c->Pcap;
   return r;
 }
 
@@ -648,6 +650,7 @@ int launch_block(isnmf_online* c, const float* dv, int64_t ldv, int nb, const ui
   a.div_first = 0;
   a.stats = c->stats;
   a.divpart = c->divpart;
+  a.stats_cap = c->maxblk;
   a.status = &c->st->status;
   a.halt = &c->st->halt;
   a.prof = c->phase_prof;
@@ -1416,6 +1419,7 @@ struct SolveWork {
       a.div_first = div_first;
       a.stats = stats_on ? stats : nullptr;
       a.divpart = divpart;
+      a.stats_cap = seg_blocks;
       a.status = &st->status;
       a.halt = halt_in ? halt_in : halt;
       if (nblk > 0) {
@@ -1461,6 +1465,7 @@ struct SolveWork {
     r.cta_part = cta_part;
     r.st = st;
     r.halt = halt;
+    r.stats_cap = seg_blocks;
     return r;
   }
 

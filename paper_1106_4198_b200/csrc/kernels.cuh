@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 
 namespace isnmf_dev {
 
@@ -77,6 +78,24 @@ struct DevState {
 // programmatic stream serialization): pdl_wait blocks until the preceding grid
 // has completed and its memory is visible (a no-op for a normal launch);
 // pdl_trigger lets the next grid start its launch before this one finishes.
+// Device-side checks of the debug build (make debug -> lib_debug/, -DISNMF_DEBUG):
+// a failed check prints its location and traps, so a bad index surfaces as a loud
+// error (compute-sanitizer is closed on this pool).  Compiled out otherwise.
+#ifdef ISNMF_DEBUG
+#define ISNMF_DASSERT(cond)                                                                          \
+  do {                                                                                               \
+    if (!(cond)) {                                                                                   \
+      printf("ISNMF_DASSERT %s:%d: %s (block %d, thread %d)\n", __FILE__, __LINE__, #cond, blockIdx.x, \
+             threadIdx.x);                                                                           \
+      __trap();                                                                                      \
+    }                                                                                                \
+  } while (0)
+#else
+#define ISNMF_DASSERT(cond) \
+  do {                      \
+  } while (0)
+#endif
+
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
@@ -154,6 +173,7 @@ struct SolveArgs {
   int check_h0;   // flag h0 <= 0 as NonPositiveInit (solve_h, kernels.hpp:67)
   float* stats;     // [gridDim][2][KP][FP], FP = F rounded up to 4
   double* divpart;  // [gridDim]
+  int stats_cap;    // planes / divergence partials allocated (debug checks; 0 = unchecked)
   unsigned int* status;
   const unsigned int* halt;
   long long* prof;  // phase cycle counters (ISNMF_PHASE_PROF builds only)
@@ -176,9 +196,13 @@ struct SolveArgs {
 constexpr float kWarmFloor = 0x1p-80f;
 
 __device__ __forceinline__ int64_t warm_col(const SolveArgs& a, int n) {  // n = launch-local frame
-  return a.widx ? int64_t(a.widx[n]) : (a.wbase + n) % a.wmod;
+  ISNMF_DASSERT(n >= 0 && n < a.nframes);
+  const int64_t col = a.widx ? int64_t(a.widx[n]) : (a.wbase + n) % a.wmod;
+  ISNMF_DASSERT(col >= 0 && col < a.wmod);
+  return col;
 }
 __device__ __forceinline__ double warm_value(const SolveArgs& a, int64_t col, uint32_t tag, int k) {
+  ISNMF_DASSERT(tag <= a.c_now && k >= 0 && k < a.K);
   return a.U[size_t(col) * a.K + k] * (a.P[size_t(a.c_now) * a.K + k] / a.P[size_t(tag) * a.K + k]);
 }
 
@@ -985,6 +1009,8 @@ struct FoldArgs {
   long long tr_cap;
   double* scale_out;  // optional: column scales s_k of this commit (batch H compensation)
   int batch_mode;
+  int stats_cap;      // planes / divergence partials allocated (debug checks; 0 = unchecked)
+  long long p_cap;    // rows of P (debug checks; 0 = unchecked)
   long long* tprof;  // ISNMF_PHASE_PROF builds: [gridDim][8] globaltimer stamps of thread 0
 };
 
@@ -1062,6 +1088,8 @@ __global__ void __cluster_dims__(kFoldCluster, 1, 1) __launch_bounds__(kFoldThre
   FOLD_T(0);
   const unsigned r = cluster_rank();
   const int k = blockIdx.x / kFoldCluster;
+  ISNMF_DASSERT(a.stats_cap == 0 || (a.nstat <= a.stats_cap && a.ndiv <= a.stats_cap));
+  ISNMF_DASSERT(a.p_cap == 0 || a.batch_mode || (long long)a.st->commits + 1 < a.p_cap);
   const int lo = int((long long)r * F / kFoldCluster), hi = int((long long)(r + 1) * F / kFoldCluster);
   const int R = fold_rows(F);
   double* sums = fsm;            // [2][F]: this rank's partial sums of column k (read by the whole cluster)

@@ -365,6 +365,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) solve_large_tc_kernel(const Sol
           }
         }
         const int FP = (F + 3) & ~3;
+        ISNMF_DASSERT(a.stats_cap == 0 || int(blockIdx.x) < a.stats_cap);
         float* outA = a.stats + size_t(blockIdx.x) * 2 * FP * KP;
         float* outB = outA + size_t(FP) * KP;
 #pragma unroll

@@ -120,6 +120,7 @@ __device__ __forceinline__ void group_sync_t(int fm) {
 // conflict-free LDS.128)
 template <int KB>
 __device__ __forceinline__ int hf_index(int n, int k) {
+  ISNMF_DASSERT(k >= 0 && k < 8 * KB && n >= 0);
   const int fm = n >> 4, nn = n & 15, kb = k >> 3, kk = k & 7;
   const int ln = 4 * (nn & 7) + (kk >> 1), ai = (nn >> 3) + 2 * (kk & 1);
   return (fm * KB + kb) * 256 + ln * 4 + ai;
@@ -663,6 +664,7 @@ __global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a
     }
     __syncthreads();
     const int FP = (F + 3) & ~3;
+    ISNMF_DASSERT(!a.stats || a.stats_cap == 0 || int(blockIdx.x) < a.stats_cap);
     float* outA = a.stats ? a.stats + size_t(blockIdx.x) * 2 * FP * KP : nullptr;
     float* outB = a.stats ? outA + size_t(FP) * KP : nullptr;
     float vv[2 * FG][4];
@@ -683,6 +685,7 @@ __global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a
   MM_STAMP(61);
   // divergence partial of this CTA (fixed-order reduction)
   if (a.divpart) {
+    ISNMF_DASSERT(a.stats_cap == 0 || int(blockIdx.x) < a.stats_cap);
     const double d = warp_sum_d(divd);
     if (lane == 0) red[warp] = d;
     __syncthreads();
