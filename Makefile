@@ -5,13 +5,14 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v --expt-r
 PKG := paper_1106_4198_b200
 LIB := $(PKG)/lib/libisnmf_b200.so
 SRC := $(PKG)/csrc/engine.cu
-TABLES := $(PKG)/csrc/mma_table.cu $(PKG)/csrc/ffma_table.cu $(PKG)/csrc/large_table.cu
-DEPS := $(wildcard $(PKG)/csrc/*.cuh) include/isnmf_b200.h
-OBJ := $(PKG)/lib/engine.o $(PKG)/lib/mma_table.o $(PKG)/lib/ffma_table.o $(PKG)/lib/large_table.o
+TABLES := $(PKG)/csrc/mma_table.cu $(PKG)/csrc/mma_multi_table.cu $(PKG)/csrc/ffma_table.cu $(PKG)/csrc/large_table.cu
+DEPS := $(wildcard $(PKG)/csrc/*.cuh) include/isnmf_b200.h $(PKG)/csrc/mma_table.cu
+OBJ := $(PKG)/lib/engine.o $(PKG)/lib/mma_table.o $(PKG)/lib/mma_multi_table.o $(PKG)/lib/ffma_table.o \
+       $(PKG)/lib/large_table.o
 
 all: $(LIB) oracle
 
-# four translation units (the engine and three kernel-instantiation tables), compiled in parallel
+# five translation units (the engine and four kernel-instantiation tables), compiled in parallel
 $(LIB): $(OBJ)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJ) -lcudart
 	@cat $(OBJ:.o=.ptxas.log) > $(PKG)/lib/ptxas.log

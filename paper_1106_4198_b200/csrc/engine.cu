@@ -32,7 +32,7 @@
 namespace isnmf_dev {
 // kernel instantiations in separate translation units (compiled in parallel):
 // K1M csrc/mma_table.cu, FFMA K1 csrc/ffma_table.cu, K1L / K1T csrc/large_table.cu
-void (*mma_kernel(int nw, int fg, int kb))(const SolveArgs);
+void (*mma_kernel(int nw, int fg, int kb, bool multi))(const SolveArgs);
 void (*ffma_kernel(int tk, int tn))(const SolveArgs);
 void (*large_kernel(int mbw, int nb))(const SolveArgs);
 void (*large_tc_kernel(int nb))(const SolveArgs);
@@ -277,6 +277,7 @@ int mma_min_frames() {
 struct SolvePlan {
   bool tiled = false;       // the kernel loops over frame tiles (K1M): any grid <= tiles works
   LargeFn large = nullptr;  // tensor-pipe kernels (large K, or the resident-dictionary variant)
+  LargeFn multi = nullptr;  // K1M's multi-tile instantiation (grid < tiles)
   int threads = 0;          // block size of `large`
   Variant* var = nullptr;  // nullptr: generic
   int NT = 0, KP = 0, WS = 0;
@@ -299,11 +300,13 @@ int plan_solve(int64_t F, int64_t K, int64_t frames, SolvePlan* plan, bool force
     const int wi = nw == 12 ? 1 : 0;
     if (nt >= mma_min_frames() && smem + 2048 <= size_t(smem_optin())) {
       if (!mma_configured[wi][fg - 1][kb - 1]) {
-        CU(cudaFuncSetAttribute(mma_kernel(nw, fg, kb), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                smem_optin() - 2048));
+        for (bool multi : {false, true})
+          CU(cudaFuncSetAttribute(mma_kernel(nw, fg, kb, multi), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  smem_optin() - 2048));
         mma_configured[wi][fg - 1][kb - 1] = true;
       }
-      plan->large = mma_kernel(nw, fg, kb);
+      plan->large = mma_kernel(nw, fg, kb, false);
+      plan->multi = mma_kernel(nw, fg, kb, true);
       plan->tiled = true;
       plan->threads = 32 * nw;
       plan->var = nullptr;
@@ -386,10 +389,11 @@ int plan_solve(int64_t F, int64_t K, int64_t frames, SolvePlan* plan, bool force
 void launch_solve(const SolvePlan& p, int nblk, const SolveArgs& args, cudaStream_t s, bool pdl = false) {
   SolveArgs a = args;
   a.cta_frames = p.NT;
-  if (p.large && pdl && pdl_enabled())
-    launch_pdl(p.large, nblk, p.threads, p.smem, s, a);
-  else if (p.large)
-    p.large<<<nblk, p.threads, p.smem, s>>>(a);
+  const LargeFn large = (p.multi && int64_t(nblk) * p.NT < a.nframes) ? p.multi : p.large;
+  if (large && pdl && pdl_enabled())
+    launch_pdl(large, nblk, p.threads, p.smem, s, a);
+  else if (large)
+    large<<<nblk, p.threads, p.smem, s>>>(a);
   else if (p.var && pdl && pdl_enabled())
     launch_pdl(p.var->fn, nblk, kThreads, p.smem, s, a);
   else if (p.var)

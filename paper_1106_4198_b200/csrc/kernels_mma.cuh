@@ -89,10 +89,10 @@ __device__ __forceinline__ int mm_rho(int n) { return n ^ (n >> 2); }
 
 // is_term (kernels.hpp:15-18) of ratio = (v+eps)/Lam as u - log(ratio) with the
 // fast log: absolute error ~1e-7 per cell (the series of is_term_ratio only
-// buys relative accuracy on terms that are themselves ~1e-7; ~2e-7 relative on a
-// 513-cell frame sum, deterministic); used for the online objective of the
-// statistics pass and for the batch objective of the incoming (W, H) (div_first),
-// whose DivergedObjective guard has 1e-6 relative slack
+// buys relative accuracy on terms that are themselves ~1e-7); used for the
+// online objective of the statistics pass.  The batch objective of the incoming
+// (W, H) (div_first) keeps the series of is_term_ratio (the fast form there makes
+// ptxas spill at the 168-register cap of the 12-warp CTA)
 __device__ __forceinline__ float is_term_fast(float ratio) {
   const float t = (ratio - 1.0f) - __logf(ratio);
   return t > 0.0f ? t : 0.0f;
@@ -201,7 +201,7 @@ __device__ __forceinline__ void mm_chunk(const float* Ws, const float* pA, const
       const float ve = vv[i][c] + eps;
       q[i][c] = valid ? ve * rr * rr : 0.0f;
       r[i][c] = valid ? rr : 0.0f;
-      if constexpr (DIV) divacc += valid ? is_term_fast(ve * rr) : 0.0f;
+      if constexpr (DIV) divacc += valid ? is_term_ratio(ve * rr) : 0.0f;
     }
   // ---- phase B: per block, K = its 8 rows (slot t <-> c0/c2, slot t+4 <-> c1/c3);
   // the dictionary values of block i+1 are loaded while block i's MMAs issue
@@ -420,7 +420,10 @@ __device__ __forceinline__ void mm_stats_block(const float* Ws, const float* Hf,
   }
 }
 
-template <int KB, int FG, int NW>
+// MULTI = false: one frame tile per CTA (online mini-batches: grid = tiles); true: CTAs
+// loop over several tiles (batch), accumulating their statistics planes and staging the
+// next tile — a separate instantiation, so the online kernel keeps its register budget
+template <int KB, int FG, int NW, bool MULTI>
 __global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a) {
   using S = MmShape<KB, FG, NW>;
   constexpr int KP = S::KP, NT = S::NT, RG = S::RG, WS = S::WS, HT = S::HT, NREG = S::NREG;
@@ -451,7 +454,7 @@ __global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a
   // frame tiles of ntc frames; CTA b owns tiles b, b + gridDim.x, ... (one tile per CTA
   // for an online mini-batch; the batch path runs one CTA per SM over all N frames, so
   // the dictionary is loaded once per CTA and the statistics planes accumulate in place)
-  const int ntiles = (a.nframes + ntc - 1) / ntc;
+  const int ntiles = MULTI ? (a.nframes + ntc - 1) / ntc : int(blockIdx.x) + 1;
 
   if (tid == 0) {  // dictionary -> smem by TMA bulk copies, overlapped with the h0 set-up below
     const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&wbar));
@@ -474,11 +477,12 @@ __global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a
   // multi-tile CTAs with direct h0 (batch): the next tile's H0 rows are staged into
   // shared memory by cp.async and its frames prefetched into L2 during this tile's
   // statistics pass (RED beyond Ht is free then)
-  const bool stage_next = a.h0_mode == 0 && !a.vsel && int(gridDim.x) < ntiles;
+  // (every tile but the last stages its successor, so tile i > 0 finds its H0 staged)
+  const bool stage_next = MULTI && a.h0_mode == 0 && !a.vsel && int(gridDim.x) < ntiles;
   float* Hstage = RED + ((KP * HT + 31) & ~31);
-  bool staged = false;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-  const bool first_tile = tile == int(blockIdx.x);
+  const bool first_tile = !MULTI || tile == int(blockIdx.x);
+  const bool staged = stage_next && !first_tile;
   const int n0 = tile * ntc;
   const int nf = min(ntc, a.nframes - n0);
   if (!first_tile) {
@@ -650,7 +654,6 @@ __global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a
       const int k = idx / NT, n = idx - k * NT;
       Ht[k * HT + n] = Hf[hf_index<KB>(n, k)];
     }
-    staged = false;
     if (stage_next && tile + int(gridDim.x) < ntiles) {
       const int n1 = (tile + int(gridDim.x)) * ntc, nf1 = min(ntc, a.nframes - n1);
       const float* src = a.H0 + size_t(n1) * K;
@@ -660,7 +663,6 @@ __global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a
       const size_t vbytes = size_t(nf1) * a.ldv * sizeof(float);
       for (size_t off = size_t(tid) * 128; off < vbytes; off += size_t(kMmThreads) * 128)
         asm volatile("prefetch.global.L2 [%0];" ::"l"(v1 + off));
-      staged = true;
     }
     __syncthreads();
     const int FP = (F + 3) & ~3;
