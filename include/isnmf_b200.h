@@ -56,7 +56,9 @@ typedef enum isnmf_status {
 enum { ISNMF_RESTART_WARM = 0, ISNMF_RESTART_FRESH = 1 };
 /* Engine flags: force the generic (W-streaming) solve kernel even when a
  * register-tiled variant would fit (testing / comparison). */
-enum { ISNMF_FLAG_GENERIC_SOLVE = 1 };
+/* solver selection: GENERIC_SOLVE = the shape-generic FP32 kernel; NO_PAIR = never the
+ * 2-SM tcgen05 kernel K1C (K1M instead); PAIR = K1C at any mini-batch size it supports */
+enum { ISNMF_FLAG_GENERIC_SOLVE = 1, ISNMF_FLAG_NO_PAIR = 2, ISNMF_FLAG_PAIR = 4 };
 
 const char* isnmf_last_error(void);
 /* Library / device description: writes a short JSON string. */
@@ -173,6 +175,9 @@ int isnmf_online_get_last_h(isnmf_online* ctx, double* h, int64_t n);
 
 /* Number of engine kernel launches issued so far (bench accounting). */
 int64_t isnmf_online_launch_count(isnmf_online* ctx);
+/* Name of the mini-batch solve kernel the context runs ("K1C", "K1M", "K1", "K1L", "K1T",
+ * "generic"), NUL-terminated into buf. */
+int isnmf_online_solver(isnmf_online* ctx, char* buf, int64_t cap);
 
 /* Profiling: begin() records a CUDA event on the engine's compute stream; with
  * per_kernel != 0 events are also recorded around every K1 (solve) and K2

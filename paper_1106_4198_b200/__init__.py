@@ -71,6 +71,7 @@ _SIGS = {
     "isnmf_online_clear_trace": ([VP], C.c_int),
     "isnmf_online_get_last_h": ([VP, VP, I64], C.c_int),
     "isnmf_online_launch_count": ([VP], I64),
+    "isnmf_online_solver": ([VP, C.c_char_p, I64], C.c_int),
     "isnmf_online_commit": ([VP], C.c_int),
     "isnmf_host_alloc": ([I64], VP),
     "isnmf_host_free": ([VP], None),
@@ -183,9 +184,11 @@ class Online:
     """Device-resident OnlineState (online.hpp:224-248) behind the C ABI."""
 
     def __init__(self, F, K, beta, inner_iters, epsilon=1e-12, restart="warm", seed=1, n_store=0, max_chunk=0,
-                 generic=False):
+                 generic=False, pair=None):
+        # pair: None = the engine's choice, False = never K1C (2-SM tcgen05 solve), True = K1C at any size
+        flags = (1 if generic else 0) | {None: 0, False: 2, True: 4}[pair]
         cfg = OnlineConfig(F=F, K=K, beta=beta, inner_iters=inner_iters, epsilon=epsilon, restart=RESTART[restart],
-                           seed=seed, n_store=n_store, max_chunk=max_chunk, flags=1 if generic else 0)
+                           seed=seed, n_store=n_store, max_chunk=max_chunk, flags=flags)
         h = C.c_void_p()
         _check(lib().isnmf_online_create(C.byref(h), C.byref(cfg)))
         self._h = h
@@ -275,6 +278,11 @@ class Online:
 
     def commit(self):
         _check(lib().isnmf_online_commit(self._h))
+
+    def solver(self):
+        buf = C.create_string_buffer(16)
+        _check(lib().isnmf_online_solver(self._h, buf, 16))
+        return buf.value.decode()
 
     def launch_count(self):
         return int(lib().isnmf_online_launch_count(self._h))

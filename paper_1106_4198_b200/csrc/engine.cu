@@ -27,6 +27,7 @@
 #include "kernels_large.cuh"
 #include "kernels_large_tc.cuh"
 #include "kernels_mma.cuh"
+#include "kernels_tc.cuh"
 #include "stft.cuh"
 
 namespace isnmf_dev {
@@ -36,12 +37,16 @@ void (*mma_kernel(int nw, int fg, int kb, bool multi))(const SolveArgs);
 void (*ffma_kernel(int tk, int tn))(const SolveArgs);
 void (*large_kernel(int mbw, int nb))(const SolveArgs);
 void (*large_tc_kernel(int nb))(const SolveArgs);
+void (*pair_kernel(int kb))(const SolveArgs);
+size_t pair_smem(int kb);
+int pc_trace_set(unsigned long long* dev_ptr);
 }  // namespace isnmf_dev
 using namespace isnmf_dev;
 
 namespace {
 
 thread_local std::string g_err;
+unsigned long long* g_trace_host = nullptr;  // isnmf_debug_pc_trace (ISNMF_PC_TRACE builds)
 
 int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -276,6 +281,7 @@ int mma_min_frames() {
 
 struct SolvePlan {
   bool tiled = false;       // the kernel loops over frame tiles (K1M): any grid <= tiles works
+  bool pair = false;        // K1C: one 2-CTA cluster per NT frames (grid = 2 x blocks, two divergence partials each)
   LargeFn large = nullptr;  // tensor-pipe kernels (large K, or the resident-dictionary variant)
   LargeFn multi = nullptr;  // K1M's multi-tile instantiation (grid < tiles)
   int threads = 0;          // block size of `large`
@@ -286,10 +292,48 @@ struct SolvePlan {
 
 bool generic_configured = false;
 
-int plan_solve(int64_t F, int64_t K, int64_t frames, SolvePlan* plan, bool force_generic = false) {
+// K1C (csrc/kernels_tc.cuh): ISNMF_K1C = 0 off, 1 (default) for mini-batches that give a
+// pair of SMs >= 40 frames, 2 at any size (tests)
+int pair_mode(int flags = 0) {
+  static const int v = [] {
+    const char* e = getenv("ISNMF_K1C");
+    return e ? atoi(e) : 1;
+  }();
+  if (flags & ISNMF_FLAG_NO_PAIR) return 0;
+  if (flags & ISNMF_FLAG_PAIR) return 2;
+  return v;
+}
+bool pair_configured[8] = {};
+
+int plan_solve(int64_t F, int64_t K, int64_t frames, SolvePlan* plan, bool force_generic = false,
+               bool allow_pair = false, int flags = 0) {
   Variant* v = nullptr;
   int WS = 0;
   size_t sm = 0;
+  const int pmode = pair_mode(flags);
+  if (allow_pair && !force_generic && pmode != 0 && K >= 17 && K <= 56 && F > 384 &&
+      F <= 2 * kPcRows + kPcMaxTail) {
+    const int pairs = device_sms() / 2;
+    const int64_t per = (frames + pairs - 1) / pairs;
+    const int np = int(std::min<int64_t>(kPcFrames, std::max<int64_t>(8, (per + 7) & ~int64_t(7))));
+    const int kb = int((K + 7) / 8);
+    const size_t smem = pair_smem(kb);
+    if ((per >= 40 || pmode == 2) && smem + 2048 <= size_t(smem_optin())) {
+      if (!pair_configured[kb]) {
+        CU(cudaFuncSetAttribute(pair_kernel(kb), cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        pair_configured[kb] = true;
+      }
+      plan->large = pair_kernel(kb);
+      plan->pair = true;
+      plan->threads = kPcThreads;
+      plan->var = nullptr;
+      plan->NT = np;
+      plan->KP = 8 * kb;
+      plan->WS = 8 * kb;
+      plan->smem = smem;
+      return 0;
+    }
+  }
   if (!force_generic && K >= 1 && K <= 56) {
     const int64_t per_cta = (frames + device_sms() - 1) / device_sms();
     const int nt = int(std::min<int64_t>(32, std::max<int64_t>(1, per_cta)));
@@ -390,6 +434,7 @@ void launch_solve(const SolvePlan& p, int nblk, const SolveArgs& args, cudaStrea
   SolveArgs a = args;
   a.cta_frames = p.NT;
   const LargeFn large = (p.multi && int64_t(nblk) * p.NT < a.nframes) ? p.multi : p.large;
+  if (p.pair) nblk *= 2;  // one 2-CTA cluster per block of NT frames
   if (large && pdl && pdl_enabled())
     launch_pdl(large, nblk, p.threads, p.smem, s, a);
   else if (large)
@@ -488,6 +533,7 @@ struct isnmf_online {
   double* P = nullptr;
   int64_t Pcap = 0;
   float* W32 = nullptr;
+  float* WB = nullptr;  // K1C layout of W^T (plan.pair only)
   float* stats = nullptr;
   double* divpart = nullptr;
   int maxblk = 0;
@@ -527,7 +573,7 @@ int online_free(isnmf_online* c) {
   if (!c) return 0;
   if (c->cs) cudaStreamSynchronize(c->cs);
   if (c->xs) cudaStreamSynchronize(c->xs);
-  void* ptrs[] = {c->st, c->W64, c->A, c->B, c->pa, c->pb, c->cta_part, c->P, c->W32, c->stats,
+  void* ptrs[] = {c->st, c->W64, c->A, c->B, c->pa, c->pb, c->cta_part, c->P, c->W32, c->WB, c->stats,
                   c->divpart, c->U, c->T, c->u01, c->Hlast, c->tr_t, c->tr_obj, c->tr_ns, c->vbuf[0],
                   c->vbuf[1], c->ibuf[0], c->ibuf[1]};
   for (void* p : ptrs) dfree(p);
@@ -604,6 +650,8 @@ FoldArgs fold_args(const isnmf_online* c) {
   r.A = c->A;
   r.B = c->B;
   r.W32 = c->W32;
+  r.WB = c->WB;
+  r.wb_kp = c->KP;
   r.P = c->P;
   r.cta_part = c->cta_part;
   r.rho = c->rho;
@@ -627,6 +675,8 @@ int launch_block(isnmf_online* c, const float* dv, int64_t ldv, int nb, const ui
   }
   SolveArgs a{};
   a.W32 = c->W32;
+  a.ws = c->WS;
+  a.WB = c->WB;
   a.F = c->F;
   a.K = c->K;
   a.V = dv;
@@ -675,7 +725,7 @@ int launch_block(isnmf_online* c, const float* dv, int64_t ldv, int nb, const ui
   const bool commit = (c->t_host + uint64_t(nb)) % uint64_t(c->beta) == 0;
   FoldArgs r = fold_args(c);
   r.nstat = nblk;
-  r.ndiv = nblk;
+  r.ndiv = c->plan.pair ? 2 * nblk : nblk;
   r.nframes = nb;
   r.do_commit = commit;
   r.eta = c->eta;
@@ -856,7 +906,8 @@ int isnmf_online_create(isnmf_online** out, const isnmf_online_config* cfg) {
   c->eps = cfg->epsilon;
   c->nstore = cfg->restart == ISNMF_RESTART_WARM ? cfg->n_store : 0;
   c->chunk = cfg->max_chunk > 0 ? cfg->max_chunk : int64_t(64) * cfg->beta;
-  int rc = plan_solve(c->F, c->K, c->beta, &c->plan, (cfg->flags & ISNMF_FLAG_GENERIC_SOLVE) != 0);
+  int rc = plan_solve(c->F, c->K, c->beta, &c->plan, (cfg->flags & ISNMF_FLAG_GENERIC_SOLVE) != 0, true,
+                      cfg->flags);
   auto bail = [&](int code) {
     std::string keep = g_err;
     online_free(c);
@@ -878,7 +929,8 @@ int isnmf_online_create(isnmf_online** out, const isnmf_online_config* cfg) {
       (rc = dalloc(&c->cta_part, size_t(fold_parts(c->K)))) ||
       (rc = dalloc(&c->W32, size_t(c->F) * c->WS)) ||
       (rc = dalloc(&c->stats, size_t(c->maxblk) * 2 * padded_f(c->F) * c->KP + 4)) ||
-      (rc = dalloc(&c->divpart, c->maxblk)) ||
+      (rc = dalloc(&c->divpart, 2 * size_t(c->maxblk))) ||
+      (c->plan.pair && (rc = dalloc(&c->WB, size_t(2) * 2 * c->KP * kWbRows))) ||
       (rc = dalloc(&c->Hlast, size_t(c->beta) * c->K)))
     return bail(rc);
   if (c->restart == ISNMF_RESTART_FRESH && (rc = dalloc(&c->u01, size_t(c->beta) * c->K))) return bail(rc);
@@ -891,6 +943,7 @@ int isnmf_online_create(isnmf_online** out, const isnmf_online_config* cfg) {
   h.kmeanw = 1.0;
   if (cudaMemcpy(c->st, &h, sizeof(h), cudaMemcpyHostToDevice) != cudaSuccess ||
       cudaMemset(c->W32, 0, size_t(c->F) * c->WS * sizeof(float)) != cudaSuccess ||
+      (c->WB && cudaMemset(c->WB, 0, size_t(2) * 2 * c->KP * kWbRows * sizeof(float)) != cudaSuccess) ||
       cudaMemset(c->pa, 0, FK * sizeof(double)) != cudaSuccess ||
       cudaMemset(c->pb, 0, FK * sizeof(double)) != cudaSuccess ||
       cudaMemset(c->Hlast, 0, size_t(c->beta) * c->K * sizeof(float)) != cudaSuccess)
@@ -925,6 +978,22 @@ int isnmf_online_set_dictionary(isnmf_online* c, const double* w, const double* 
         sum += w[k * F + f];
       }
     CU(cudaMemcpy(c->W32, w32.data(), w32.size() * sizeof(float), cudaMemcpyHostToDevice));
+    if (c->WB) {  // K1C's W^T halves (the layout K2 keeps up to date at every commit)
+      std::vector<float> wb(size_t(2) * 2 * c->KP * kWbRows, 0.0f);
+      for (int64_t k = 0; k < K; ++k)
+        for (int64_t f = 0; f < std::min<int64_t>(F, 2 * kWbRows); ++f) {
+          const float x = w32[f * c->WS + k];
+          float hi;
+          uint32_t u;
+          std::memcpy(&u, &x, 4);
+          u &= 0xffffe000u;
+          std::memcpy(&hi, &u, 4);
+          const size_t half = size_t(f / kWbRows) * 2 * c->KP * kWbRows;
+          wb[half + wb_offset(int(k), int(f % kWbRows))] = x;
+          wb[half + wb_offset(c->KP + int(k), int(f % kWbRows))] = x - hi;
+        }
+      CU(cudaMemcpy(c->WB, wb.data(), wb.size() * sizeof(float), cudaMemcpyHostToDevice));
+    }
     const double kmeanw = double(K) * (sum / double(F * K));
     CU(cudaMemcpy(reinterpret_cast<char*>(c->st) + offsetof(DevState, kmeanw), &kmeanw, sizeof(double),
                   cudaMemcpyHostToDevice));
@@ -1151,6 +1220,38 @@ int isnmf_online_get_last_h(isnmf_online* c, double* h, int64_t n) {
 }
 
 int64_t isnmf_online_launch_count(isnmf_online* c) { return c ? c->launches : -1; }
+
+int isnmf_online_solver(isnmf_online* c, char* buf, int64_t cap) {
+  if (!c || !buf || cap < 1) return fail(ISNMF_E_INVALID_ARG, "online_solver: NULL argument");
+  const SolvePlan& p = c->plan;
+  const char* name = p.pair                                      ? "K1C"
+                     : p.tiled                                   ? "K1M"
+                     : p.var                                     ? "K1"
+                     : p.large && p.threads == kTcThreads        ? "K1T"
+                     : p.large                                   ? "K1L"
+                                                                 : "generic";
+  std::snprintf(buf, size_t(cap), "%s", name);
+  return 0;
+}
+
+#ifdef ISNMF_PC_TRACE
+// K1C progress trace (ISNMF_PC_TRACE builds, `make trace`): maps a host buffer of cap
+// words the kernel writes its per-warp progress into; read it with out != NULL at any
+// time (no synchronisation: the point is to see where a stuck launch waits)
+int isnmf_debug_pc_trace(long long* out, int64_t cap) {
+  if (!g_trace_host) {
+    CU(cudaHostAlloc(reinterpret_cast<void**>(&g_trace_host), size_t(cap) * 8, cudaHostAllocMapped));
+    std::memset(g_trace_host, 0, size_t(cap) * 8);
+    unsigned long long* dp = nullptr;
+    CU(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dp), g_trace_host, 0));
+    if (pc_trace_set(dp)) return fail(ISNMF_E_UNSUPPORTED, "not an ISNMF_PC_TRACE build");
+    return 0;
+  }
+  if (out) std::memcpy(out, g_trace_host, size_t(cap) * 8);
+  return 0;
+}
+
+#endif
 
 #ifdef ISNMF_PHASE_PROF
 // Debug hook of ISNMF_PHASE_PROF builds: per-(CTA, warp) cycles per K1 phase.

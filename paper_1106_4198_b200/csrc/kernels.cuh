@@ -144,6 +144,8 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 // ---------------------------------------------------------------------------
 struct SolveArgs {
   const float* W32;  // [F][SolveShape::WS], pad columns zero
+  int ws;            // row stride of W32 (floats)
+  const float* WB;   // K1C: W^T hi | lo in its K-major halves (pc_off_wb), nullable otherwise
   int F, K;
   const float* V;  // frames; block-local frame n is V + frame(n) * ldv
   int64_t ldv;
@@ -983,6 +985,13 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
   return t;
 }
 
+// K1C (csrc/kernels_tc.cuh) layout of one CTA's half of W^T: K-major without swizzle,
+// N = k' (hi k | lo k), K = row, core matrices of 8 k' x 4 rows
+constexpr int kWbRows = 256;
+__host__ __device__ __forceinline__ int wb_offset(int kp, int row) {
+  return (((kp >> 3) * (kWbRows / 4) + (row >> 2)) << 5) + ((kp & 7) << 2) + (row & 3);
+}
+
 struct FoldArgs {
   const float* stats;  // [nblk][2][KP][FP]
   const double* divpart;
@@ -996,6 +1005,8 @@ struct FoldArgs {
   double* A;
   double* B;
   float* W32;
+  float* WB;         // optional: the K1C layout of W^T (hi | lo, pc_off_wb), kp rows per half
+  int wb_kp;
   double* P;         // prefix products of the column scales [commits+1][K]
   double* cta_part;  // [gridDim][2]: dW^2, sum W of this CTA
   int do_commit;
@@ -1088,7 +1099,7 @@ __global__ void __cluster_dims__(kFoldCluster, 1, 1) __launch_bounds__(kFoldThre
   FOLD_T(0);
   const unsigned r = cluster_rank();
   const int k = blockIdx.x / kFoldCluster;
-  ISNMF_DASSERT(a.stats_cap == 0 || (a.nstat <= a.stats_cap && a.ndiv <= a.stats_cap));
+  ISNMF_DASSERT(a.stats_cap == 0 || (a.nstat <= a.stats_cap && a.ndiv <= 2 * a.stats_cap));
   ISNMF_DASSERT(a.p_cap == 0 || a.batch_mode || (long long)a.st->commits + 1 < a.p_cap);
   const int lo = int((long long)r * F / kFoldCluster), hi = int((long long)(r + 1) * F / kFoldCluster);
   const int R = fold_rows(F);
@@ -1250,7 +1261,13 @@ __global__ void __cluster_dims__(kFoldCluster, 1, 1) __launch_bounds__(kFoldThre
     a.W64[cell] = wn;
     a.A[cell] = rpa[j] / sc;
     a.B[cell] = rpb[j] * sc;
-    a.W32[size_t(f) * a.WS + k] = float(wn);
+    const float w32 = float(wn);
+    a.W32[size_t(f) * a.WS + k] = w32;
+    if (a.WB && f < 2 * kWbRows) {  // K1C's W^T halves: hi = the fp32 value, lo = its tf32 remainder
+      const size_t half = size_t(f / kWbRows) * 2 * a.wb_kp * kWbRows;
+      a.WB[half + wb_offset(k, f % kWbRows)] = w32;
+      a.WB[half + wb_offset(a.wb_kp + k, f % kWbRows)] = w32 - __uint_as_float(__float_as_uint(w32) & 0xffffe000u);
+    }
   }
   if (ok && r == 0 && tid == 0) {
     const unsigned long long c = a.st->commits;
