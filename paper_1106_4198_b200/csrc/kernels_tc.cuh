@@ -40,9 +40,13 @@ namespace isnmf_dev {
 constexpr int kPcRows = 256;    // dictionary rows per CTA
 constexpr int kPcFrames = 64;   // frames of a pair (phase-A N, half of phase-B M)
 constexpr int kPcEpiWarps = 8;  // epilogue warps: (quarter q = warp & 3, frame half hh = warp >> 2)
-constexpr int kPcIssueWarp = 8;
-constexpr int kPcTailWarp = 9;
-constexpr int kPcThreads = 320;
+constexpr int kPcIssueWarp = 0; // its lane 0 also issues every MMA, between its epilogue steps
+constexpr int kPcTailWarp = 7;  // also the FP32 tail rows (quarter 3 waits for a slot first)
+constexpr int kPcThreads = 256; // two warps per SM sub-partition: 255 registers, v + eps resident
+// chunk issue order within a tile: quarters 0, 1, 2, 3 (the issuing warp stages the first)
+__host__ __device__ constexpr int pc_chunk_quarter(int i) { return i & 3; }
+__host__ __device__ constexpr int pc_quarter_chunk(int q) { return q & 3; }
+constexpr int kPcIssueBefore = 0;  // chunks of a tile the issuer issues before staging its own
 constexpr int kPcMaxTail = 8;   // rows >= 512 on the FP32 pipe
 constexpr int kPcSlotFloats = 2 * 128 * 32;
 
@@ -114,6 +118,27 @@ __device__ __forceinline__ uint32_t dsmem_addr(const void* p, uint32_t rank) {
   uint32_t r;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr(p)), "r"(rank));
   return r;
+}
+// arrive on the mbarrier at the same offset in the peer CTA (release, cluster scope)
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t rank) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(dsmem_addr(bar, rank))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done)
+    asm volatile(
+        "{\n\t.reg .pred P;\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%1], %2;\n\tselp.b32 %0, 1, "
+        "0, P;\n\t}\n"
+        : "=r"(done)
+        : "r"(smem_addr(bar)), "r"(parity)
+        : "memory");
 }
 __device__ __forceinline__ void dsmem_st4(uint32_t addr, float4 v) {
   asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
@@ -197,14 +222,15 @@ __device__ __forceinline__ float tf32_lo(float x) { return x - __uint_as_float(_
 // host memory (readable while the kernel runs): [CTA][warp] = pass << 24 | site << 16 | arg
 #ifdef ISNMF_PC_TRACE
 static __device__ unsigned long long* g_pc_trace = nullptr;  // (tc_table.cu's copy is set)
+// per-warp timeline of CTAs 0 and 1 in shared memory (a store to sysmem before a
+// barrier.cluster.arrive.release would be waited for), dumped at the end of the launch to
+// g_pc_trace[4096 + (cta * 10 + warp) * 512 ..]: clock64 << 16 | site << 8 | (arg & 0xff)
+constexpr int kPcLog = 96;
 #define PC_MARK(site, arg)                                                                            \
   do {                                                                                                \
-    if ((threadIdx.x & 31) == 0 && g_pc_trace) {                                                      \
-      *reinterpret_cast<volatile unsigned long long*>(g_pc_trace + blockIdx.x * 10 + (threadIdx.x >> 5)) = \
-          (1ull << 56) | (unsigned long long)(pass_no & 0xff) << 24 | (unsigned long long)(site) << 16 |      \
-          (unsigned long long)((arg) & 0xffff);                                                       \
-      __threadfence_system();                                                                         \
-    }                                                                                                 \
+    if ((threadIdx.x & 31) == 0 && pc_n < kPcLog)                                                     \
+      pc_log[(threadIdx.x >> 5) * kPcLog + pc_n++] =                                                  \
+          (unsigned long long)clock64() << 16 | (unsigned long long)(site) << 8 | ((arg) & 0xff);     \
   } while (0)
 #else
 #define PC_MARK(site, arg)
@@ -235,6 +261,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPcThreads, 1) solve
   __shared__ uint32_t s_tmem;
   // bar_full / bar_empty per chunk (each completes once a pass, so a parity wait is exact)
   __shared__ __align__(8) uint64_t bar_w, bar_a[2], bar_full[8], bar_empty[8], bar_b, bar_sa, bar_s;
+  // exchange: bar_pfree = the peer's phase B is done (its slots take our partials), bar_xfull =
+  // the peer's partials have landed in our slots (bulk copy, complete_tx)
+  __shared__ __align__(8) uint64_t bar_pfree, bar_xfull;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t rank = cluster_ctarank(), peer = rank ^ 1u;
@@ -245,8 +274,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPcThreads, 1) solve
   const int rowF = min(F, 2 * kPcRows);          // rows on the tensor cores: [0, rowF)
   const int ntail = F > 2 * kPcRows ? F - 2 * kPcRows : 0;
   const float eps = a.eps;
-  int pass_no = 0;
+  int pass_no = 0, pc_n = 0;
   (void)pass_no;
+  (void)pc_n;
+#ifdef ISNMF_PC_TRACE
+  __shared__ unsigned long long pc_log[(kPcThreads / 32) * kPcLog];
+#endif
 
   pdl_wait();
   if (warp == kPcIssueWarp) {
@@ -267,6 +300,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPcThreads, 1) solve
     mbar_init(&bar_b, 1);
     mbar_init(&bar_sa, 32 * kPcEpiWarps);
     mbar_init(&bar_s, 1);
+    mbar_init(&bar_pfree, 1);
+    mbar_init(&bar_xfull, 1);  // thread 0's arrive.expect_tx + the peer's bulk copy
     asm volatile("fence.mbarrier_init.release.cluster;");
     if (s_go) {  // this CTA's half of W^T by TMA bulk copies
       const uint32_t bytes = uint32_t(S::WB_FLOATS) * 4u;
@@ -375,6 +410,123 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPcThreads, 1) solve
   const int q = warp & 3, hh = (warp >> 2) & 1;
   const uint32_t tlane = tmem + (uint32_t(32 * q) << 16);
   float divacc = 0.0f;
+  // ---- MMA issue (lane 0 of warp kPcIssueWarp, in program order between its epilogue steps)
+  auto issue_phase_a = [&](int t) {  // tile t: D_A[t] = W_hi h_hi + W_hi h_lo + W_lo h_hi
+    tc_fence_after();
+    constexpr uint32_t idA = umma_idesc_tf32(128, kPcFrames, 0, 0);
+    const uint32_t d = tmem + S::C_DA + uint32_t(64 * t);
+#pragma unroll
+    for (int s = 0; s < KB; ++s) {
+      const uint32_t ahi = tmem + uint32_t(t * KP2 + 8 * s), alo = ahi + KP;
+      const uint64_t bh = umma_desc(smem_addr(Hh + 64 * s), 128, (KP / 4) * 128, 0);
+      const uint64_t bl = umma_desc(smem_addr(Hl + 64 * s), 128, (KP / 4) * 128, 0);
+      umma_ts(d, ahi, bh, idA, s > 0 ? 1u : 0u);
+      umma_ts(d, ahi, bl, idA, 1u);
+      umma_ts(d, alo, bh, idA, 1u);
+    }
+    umma_commit(&bar_a[t]);
+  };
+  // phase B of chunks c0 .. c0 + n - 1 (issue order: tile c / 4, quarter pc_chunk_quarter(c % 4)),
+  // each once its slot is staged
+  auto issue_chunks = [&](int c0, int n, int pass) {
+    constexpr uint32_t id1 = umma_idesc_tf32(128, KP2, 1, 0), id2 = umma_idesc_tf32(128, NHI, 1, 0);
+#pragma unroll 1
+    for (int c = c0; c < c0 + n; ++c) {
+      const int sl = c & 1, t = c >> 2, qq = pc_chunk_quarter(c & 3);
+      PC_MARK(21, c);
+      mbar_wait(&bar_full[c], pass & 1);
+      PC_MARK(22, c);
+      tc_fence_after();
+      const float* op0 = slot + sl * kPcSlotFloats;
+      const float* op1 = op0 + kPcSlotFloats / 2;
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        const int row0 = 128 * t + 32 * qq + 8 * s;
+        const uint64_t a0 = umma_desc(smem_addr(op0 + 2 * s * 4 * 128), 512, 4 * 512, 1);
+        const uint64_t a1 = umma_desc(smem_addr(op1 + 2 * s * 4 * 128), 512, 4 * 512, 1);
+        const uint64_t bw = umma_desc(smem_addr(WB + (row0 >> 2) * 32), 128, (kPcRows / 4) * 128, 0);
+        umma_tf32(tmem + S::C_DB, a0, bw, id1, (c > 0 || s > 0) ? 1u : 0u);
+        umma_tf32(tmem + S::C_DB, a1, bw, id2, 1u);
+      }
+      umma_commit(&bar_empty[c]);
+    }
+    if (c0 + n == 8) {
+      umma_commit(&bar_b);
+      PC_MARK(23, 0);
+    }
+  };
+  // statistics MMAs of tile t once every thread has written its A_S columns
+  auto issue_stats = [&](int t) {
+    constexpr uint32_t idS = umma_idesc_tf32(128, NHI, 0, 0);
+    PC_MARK(24, t);
+    mbar_wait(&bar_sa, t & 1);
+    PC_MARK(25, t);
+    tc_fence_after();
+#pragma unroll
+    for (int s = 0; s < kPcFrames / 8; ++s) {
+      const uint64_t bh = umma_desc(smem_addr(HT + 64 * s), 128, (kPcFrames / 4) * 128, 0);
+      const uint64_t bl =
+          umma_desc(smem_addr(HT + (KP / 8) * (kPcFrames / 4) * 32 + 64 * s), 128, (kPcFrames / 4) * 128, 0);
+      const uint32_t qh = tmem + S::C_AS + 8 * s, ql = qh + 64, rh = qh + 128, rl = qh + 192;
+      const uint32_t da = tmem + S::C_DS, db = da + 64;
+      umma_ts(da, qh, bh, idS, s > 0 ? 1u : 0u);
+      umma_ts(da, qh, bl, idS, 1u);
+      umma_ts(da, ql, bh, idS, 1u);
+      umma_ts(db, rh, bh, idS, s > 0 ? 1u : 0u);
+      umma_ts(db, rh, bl, idS, 1u);
+      umma_ts(db, rl, bh, idS, 1u);
+    }
+    umma_commit(&bar_s);
+  };
+
+  // rows >= 512 on the FP32 pipe (lanes 1..31 of the issuer warp, beside the MMA issue):
+  // q / r of every frame for the update, and in the statistics pass their plane rows
+  auto tail_rows = [&](int l, int nl, bool stats_pass) {
+    for (int i = 0; i < ntail; ++i) {
+      const int row = 2 * kPcRows + i;
+      for (int n = l; n < kPcFrames; n += nl) {
+        float lam = 0.0f;
+#pragma unroll
+        for (int k = 0; k < KP; ++k) lam = fmaf(Wt[i * KP + k], Hh[pc_off_h<KP>(n, k)], lam);
+        const bool valid = n < nf;
+        const float rr = rcp_approx(lam + eps);
+        const float ve = (valid ? __ldg(fptr[n] + row) : 0.0f) + eps;
+        Qt[i * kPcFrames + n] = valid ? ve * rr * rr : 0.0f;
+        Rt[i * kPcFrames + n] = valid ? rr : 0.0f;
+        if (stats_pass && rank == 1 && valid) divacc += is_term_fast(ve * rr);
+      }
+    }
+  };
+  auto tail_stats = [&](int l, int nl) {  // rank 1: the tail rows of the pair's statistics plane
+    const int FP = (F + 3) & ~3;
+    float* outA = a.stats + size_t(pair) * 2 * FP * KP;
+    float* outB = outA + size_t(FP) * KP;
+    for (int idx = l; idx < ntail * K; idx += nl) {
+      const int i = idx / K, k = idx - i * K;
+      float sa = 0.0f, sb = 0.0f;
+      for (int n = 0; n < kPcFrames; ++n) {
+        const float h = Hh[pc_off_h<KP>(n, k)];
+        sa = fmaf(Qt[i * kPcFrames + n], h, sa);
+        sb = fmaf(Rt[i * kPcFrames + n], h, sb);
+      }
+      outA[size_t(k) * FP + 2 * kPcRows + i] = sa;
+      outB[size_t(k) * FP + 2 * kPcRows + i] = sb;
+    }
+  };
+
+  // v + eps of this thread's cells (rows 128t + 32q + lane, frames 32hh ..), resident for every pass
+  float vr[2][32];
+  if (warp < kPcEpiWarps) {
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const int row = int(rank) * kPcRows + 128 * t + 32 * q + lane;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int n = 32 * hh + j;
+        vr[t][j] = (row < rowF && n < nf ? __ldg(fptr[n] + row) : 0.0f) + eps;
+      }
+    }
+  }
   const int passes = a.iters + 1;
   for (int pass = 0; pass < passes; ++pass) {
     const bool stats_pass = pass == a.iters;
@@ -401,135 +553,41 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPcThreads, 1) solve
       proxy_fence();
       __syncthreads();
     }
-    // ------------------------------------------------------------------ issuer
-    if (warp == kPcIssueWarp) {
+    // ------------------------------------------------------------------ issuer (+ tail rows)
+    if (warp == kPcIssueWarp) {  // tile 0 now; tile 1 once the first chunk is queued
       if (lane == 0) {
-        tc_fence_after();
-        constexpr uint32_t idA = umma_idesc_tf32(128, kPcFrames, 0, 0);
-#pragma unroll 1
-        for (int t = 0; t < 2; ++t) {
-          const uint32_t d = tmem + S::C_DA + uint32_t(64 * t);
-#pragma unroll
-          for (int s = 0; s < KB; ++s) {
-            const uint32_t ahi = tmem + uint32_t(t * KP2 + 8 * s), alo = ahi + KP;
-            const uint64_t bh = umma_desc(smem_addr(Hh + 64 * s), 128, (KP / 4) * 128, 0);
-            const uint64_t bl = umma_desc(smem_addr(Hl + 64 * s), 128, (KP / 4) * 128, 0);
-            umma_ts(d, ahi, bh, idA, s > 0 ? 1u : 0u);
-            umma_ts(d, ahi, bl, idA, 1u);
-            umma_ts(d, alo, bh, idA, 1u);
-          }
-          umma_commit(&bar_a[t]);
-        }
-        if (!stats_pass) {
-          constexpr uint32_t id1 = umma_idesc_tf32(128, KP2, 1, 0), id2 = umma_idesc_tf32(128, NHI, 1, 0);
-#pragma unroll 1
-          for (int c = 0; c < 8; ++c) {
-            const int sl = c & 1, t = c >> 2, qq = c & 3;
-            PC_MARK(21, c);
-            mbar_wait(&bar_full[c], pass & 1);
-            PC_MARK(22, c);
-            tc_fence_after();
-            const float* op0 = slot + sl * kPcSlotFloats;
-            const float* op1 = op0 + kPcSlotFloats / 2;
-#pragma unroll
-            for (int s = 0; s < 4; ++s) {
-              const int row0 = 128 * t + 32 * qq + 8 * s;
-              const uint64_t a0 = umma_desc(smem_addr(op0 + 2 * s * 4 * 128), 512, 4 * 512, 1);
-              const uint64_t a1 = umma_desc(smem_addr(op1 + 2 * s * 4 * 128), 512, 4 * 512, 1);
-              const uint64_t bw = umma_desc(smem_addr(WB + (row0 >> 2) * 32), 128, (kPcRows / 4) * 128, 0);
-              umma_tf32(tmem + S::C_DB, a0, bw, id1, (c > 0 || s > 0) ? 1u : 0u);
-              umma_tf32(tmem + S::C_DB, a1, bw, id2, 1u);
-            }
-            umma_commit(&bar_empty[c]);
-          }
-          umma_commit(&bar_b);
-          PC_MARK(23, 0);
-        } else {
-          constexpr uint32_t idS = umma_idesc_tf32(128, NHI, 0, 0);
-#pragma unroll 1
-          for (int t = 0; t < 2; ++t) {
-            PC_MARK(24, t);
-            mbar_wait(&bar_sa, t & 1);
-            PC_MARK(25, t);
-            tc_fence_after();
-#pragma unroll
-            for (int s = 0; s < kPcFrames / 8; ++s) {
-              const uint64_t bh = umma_desc(smem_addr(HT + 64 * s), 128, (kPcFrames / 4) * 128, 0);
-              const uint64_t bl = umma_desc(smem_addr(HT + (KP / 8) * (kPcFrames / 4) * 32 + 64 * s), 128,
-                                            (kPcFrames / 4) * 128, 0);
-              const uint32_t qh = tmem + S::C_AS + 8 * s, ql = qh + 64, rh = qh + 128, rl = qh + 192;
-              const uint32_t da = tmem + S::C_DS, db = da + 64;
-              umma_ts(da, qh, bh, idS, s > 0 ? 1u : 0u);
-              umma_ts(da, qh, bl, idS, 1u);
-              umma_ts(da, ql, bh, idS, 1u);
-              umma_ts(db, rh, bh, idS, s > 0 ? 1u : 0u);
-              umma_ts(db, rh, bl, idS, 1u);
-              umma_ts(db, rl, bh, idS, 1u);
-            }
-            umma_commit(&bar_s);
-          }
-        }
+        issue_phase_a(0);
+        if (stats_pass) issue_phase_a(1);
       }
       __syncwarp();
     }
-    // ------------------------------------------------------------------ tail rows (FP32)
     if (warp == kPcTailWarp && ntail > 0) {
-      for (int i = 0; i < ntail; ++i) {
-        const int row = 2 * kPcRows + i;
-#pragma unroll
-        for (int hn = 0; hn < 2; ++hn) {
-          const int n = lane + 32 * hn;
-          float lam = 0.0f;
-#pragma unroll
-          for (int k = 0; k < KP; ++k) lam = fmaf(Wt[i * KP + k], Hh[pc_off_h<KP>(n, k)], lam);
-          const bool valid = n < nf;
-          const float rr = rcp_approx(lam + eps);
-          const float ve = (valid ? __ldg(fptr[n] + row) : 0.0f) + eps;
-          Qt[i * kPcFrames + n] = valid ? ve * rr * rr : 0.0f;
-          Rt[i * kPcFrames + n] = valid ? rr : 0.0f;
-          if (stats_pass && rank == 1 && valid) divacc += is_term_fast(ve * rr);
-        }
+      tail_rows(lane, 32, stats_pass);
+      if (stats_pass && rank == 1 && a.stats) {
+        __syncwarp();
+        tail_stats(lane, 32);
       }
       __syncwarp();
-      if (stats_pass && rank == 1 && a.stats) {  // tail rows of the statistics plane
-        const int FP = (F + 3) & ~3;
-        float* outA = a.stats + size_t(pair) * 2 * FP * KP;
-        float* outB = outA + size_t(FP) * KP;
-        for (int idx = lane; idx < ntail * K; idx += 32) {
-          const int i = idx / K, k = idx - i * K;
-          float sa = 0.0f, sb = 0.0f;
-          for (int n = 0; n < kPcFrames; ++n) {
-            const float h = Hh[pc_off_h<KP>(n, k)];
-            sa = fmaf(Qt[i * kPcFrames + n], h, sa);
-            sb = fmaf(Rt[i * kPcFrames + n], h, sb);
-          }
-          outA[size_t(k) * FP + 2 * kPcRows + i] = sa;
-          outB[size_t(k) * FP + 2 * kPcRows + i] = sb;
-        }
-      }
     }
     // ------------------------------------------------------------------ epilogue warps
     if (warp < kPcEpiWarps) {
-#pragma unroll 1
+#pragma unroll
       for (int t = 0; t < 2; ++t) {
         const int row = int(rank) * kPcRows + 128 * t + 32 * q + lane;
         const bool rowok = row < rowF;
-        float v[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int n = 32 * hh + j;
-          v[j] = (rowok && n < nf) ? __ldg(fptr[n] + row) : 0.0f;
-        }
+        const float* v = vr[t];
         PC_MARK(2, t);
         mbar_wait(&bar_a[t], pass & 1);
         PC_MARK(3, t);
         tc_fence_after();
-        float lam[32];
-        tmem_ld<32>(tlane + S::C_DA + uint32_t(64 * t + 32 * hh), lam);
-        tmem_ld_wait();
+        const uint32_t cA = tlane + S::C_DA + uint32_t(64 * t + 32 * hh);
         if (!stats_pass) {
           // slot sl = c & 1 last held chunk c - 2 (or chunk c + 6 of the previous pass)
-          const int c = 4 * t + q, sl = c & 1;
+          const int c = 4 * t + pc_quarter_chunk(q), sl = c & 1;
+          if (kPcIssueBefore > 0 && warp == kPcIssueWarp) {  // chunks ahead of our own
+            if (lane == 0) issue_chunks(4 * t, kPcIssueBefore, pass);
+            __syncwarp();
+          }
           PC_MARK(4, c);
           if (c >= 2)
             mbar_wait(&bar_empty[c - 2], pass & 1);
@@ -538,32 +596,48 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPcThreads, 1) solve
           PC_MARK(5, c);
           float* op0 = slot + sl * kPcSlotFloats;
           float* op1 = op0 + kPcSlotFloats / 2;
-          const int sw = (lane >> 2) & 1;  // conflict-free order of the 16-byte m quads
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int ii = i ^ sw;
-            float qv[4], rv[4];
+          for (int hf = 0; hf < 2; ++hf) {  // 16 frames at a time (register budget: 3 warps / SMSP)
+            float lam[16];
+            tmem_ld<16>(cA + 16 * hf, lam);
+            tmem_ld_wait();
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const int j = 4 * ii + e, n = 32 * hh + j;
-              const bool valid = rowok && n < nf;
-              const float rr = rcp_approx(lam[j] + eps);
-              const float ve = v[j] + eps;
-              qv[e] = valid ? ve * rr * rr : 0.0f;
-              rv[e] = valid ? rr : 0.0f;
+            for (int i = 0; i < 4; ++i) {
+              float qv[4], rv[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const int j = 16 * hf + 4 * i + e, n = 32 * hh + j;
+                const bool valid = rowok && n < nf;
+                const float rr = rcp_approx(lam[4 * i + e] + eps);
+                qv[e] = valid ? v[j] * rr * rr : 0.0f;
+                rv[e] = valid ? rr : 0.0f;
+              }
+              const int mq = 32 * hh + 16 * hf + 4 * i;
+              const int oq = pc_off_st(mq, lane), orr = pc_off_st(64 + mq, lane);
+              *reinterpret_cast<float4*>(op0 + oq) = make_float4(qv[0], qv[1], qv[2], qv[3]);
+              *reinterpret_cast<float4*>(op0 + orr) = make_float4(rv[0], rv[1], rv[2], rv[3]);
+              *reinterpret_cast<float4*>(op1 + oq) =
+                  make_float4(tf32_lo(qv[0]), tf32_lo(qv[1]), tf32_lo(qv[2]), tf32_lo(qv[3]));
+              *reinterpret_cast<float4*>(op1 + orr) =
+                  make_float4(tf32_lo(rv[0]), tf32_lo(rv[1]), tf32_lo(rv[2]), tf32_lo(rv[3]));
             }
-            const int mq = 32 * hh + 4 * ii;
-            const int oq = pc_off_st(mq, lane), orr = pc_off_st(64 + mq, lane);
-            *reinterpret_cast<float4*>(op0 + oq) = make_float4(qv[0], qv[1], qv[2], qv[3]);
-            *reinterpret_cast<float4*>(op0 + orr) = make_float4(rv[0], rv[1], rv[2], rv[3]);
-            *reinterpret_cast<float4*>(op1 + oq) =
-                make_float4(tf32_lo(qv[0]), tf32_lo(qv[1]), tf32_lo(qv[2]), tf32_lo(qv[3]));
-            *reinterpret_cast<float4*>(op1 + orr) =
-                make_float4(tf32_lo(rv[0]), tf32_lo(rv[1]), tf32_lo(rv[2]), tf32_lo(rv[3]));
           }
           proxy_fence();
           mbar_arrive(&bar_full[c]);
           PC_MARK(6, c);
+          if (warp == kPcIssueWarp) {  // the rest of the tile's chunks, in order
+            if (lane == 0) {
+              if (t == 0) {  // our chunk (the tile's first), then phase A of tile 1 behind it
+                issue_chunks(kPcIssueBefore, 1, pass);
+                issue_phase_a(1);
+                issue_chunks(kPcIssueBefore + 1, 3 - kPcIssueBefore, pass);
+              } else {
+                issue_chunks(4 + kPcIssueBefore, 4 - kPcIssueBefore, pass);
+              }
+            }
+            __syncwarp();
+          }
+
         } else {
           // statistics pass: q / r (hi | lo) of this tile into TMEM as the A operands (A_S
           // overlays W_A: both tiles' phase-A MMAs must be done; for tile 1 the tile-0
@@ -572,52 +646,61 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPcThreads, 1) solve
             mbar_wait(&bar_a[1], pass & 1);
             tc_fence_after();
           }
-          float x[32];
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int n = 32 * hh + j;
-            const bool valid = rowok && n < nf;
-            const float rr = rcp_approx(lam[j] + eps);
-            const float ve = v[j] + eps;
-            if (valid) divacc += is_term_fast(ve * rr);
-            x[j] = valid ? ve * rr * rr : 0.0f;   // q
-            lam[j] = valid ? rr : 0.0f;           // r
+          for (int hf = 0; hf < 2; ++hf) {
+            float lam[16], x[16];
+            tmem_ld<16>(cA + 16 * hf, lam);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const int n = 32 * hh + 16 * hf + j;
+              const bool valid = rowok && n < nf;
+              const float rr = rcp_approx(lam[j] + eps);
+              const float ve = v[16 * hf + j];
+              if (valid) divacc += is_term_fast(ve * rr);
+              x[j] = valid ? ve * rr * rr : 0.0f;  // q
+              lam[j] = valid ? rr : 0.0f;          // r
+            }
+            const uint32_t ca = tlane + S::C_AS + uint32_t(32 * hh + 16 * hf);
+            tmem_st<16>(ca, x);
+            tmem_st<16>(ca + 128, lam);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              x[j] = tf32_lo(x[j]);
+              lam[j] = tf32_lo(lam[j]);
+            }
+            tmem_st<16>(ca + 64, x);
+            tmem_st<16>(ca + 192, lam);
           }
-          const uint32_t ca = tlane + S::C_AS + uint32_t(32 * hh);
-          tmem_st_n<32>(ca, x);
-#pragma unroll
-          for (int j = 0; j < 32; ++j) x[j] = tf32_lo(x[j]);
-          tmem_st_n<32>(ca + 64, x);
-          tmem_st_n<32>(ca + 128, lam);
-#pragma unroll
-          for (int j = 0; j < 32; ++j) lam[j] = tf32_lo(lam[j]);
-          tmem_st_n<32>(ca + 192, lam);
           tmem_st_wait();
           tc_fence_before();
           mbar_arrive(&bar_sa);
           PC_MARK(10, t);
+          if (warp == kPcIssueWarp) {
+            if (lane == 0) issue_stats(t);
+            __syncwarp();
+          }
+
           // statistics of this tile -> the pair's plane (rows of this CTA)
           mbar_wait(&bar_s, t & 1);
           PC_MARK(11, t);
           tc_fence_after();
-          float sa[KH], sb[KH];
-          tmem_ld_n<KH>(tlane + S::C_DS + uint32_t(KH * hh), sa);
-          tmem_ld_n<KH>(tlane + S::C_DS + 64 + uint32_t(KH * hh), sb);
-          tmem_ld_wait();
-          tc_fence_before();
-          if (a.stats && rowok) {
-            const int FP = (F + 3) & ~3;
-            float* outA = a.stats + size_t(pair) * 2 * FP * KP;
-            float* outB = outA + size_t(FP) * KP;
+          const int FP = (F + 3) & ~3;
+          float* out = a.stats ? a.stats + size_t(pair) * 2 * FP * KP : nullptr;
 #pragma unroll
-            for (int j = 0; j < KH; ++j) {
-              const int k = KH * hh + j;
-              if (k < K) {
-                outA[size_t(k) * FP + row] = sa[j];
-                outB[size_t(k) * FP + row] = sb[j];
+          for (int ab = 0; ab < 2; ++ab) {  // sa, then sb
+            float sv[KH];
+            tmem_ld_n<KH>(tlane + S::C_DS + uint32_t(64 * ab + KH * hh), sv);
+            tmem_ld_wait();
+            if (out && rowok) {
+#pragma unroll
+              for (int j = 0; j < KH; ++j) {
+                const int k = KH * hh + j;
+                if (k < K) out[size_t(ab) * FP * KP + size_t(k) * FP + row] = sv[j];
               }
             }
           }
+          tc_fence_before();
         }
       }
     }
@@ -631,37 +714,52 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPcThreads, 1) solve
       tc_fence_after();
     }
     PC_MARK(8, 0);
-    cluster_arrive();  // this CTA's phase B is done: the peer may overwrite the slots with its partials
-    if (warp < kPcEpiWarps) {
-      float x[KH], y[KH];
-      const uint32_t cb = tlane + S::C_DB + uint32_t(KH * hh);
-      tmem_ld_n<KH>(cb, x);
-      tmem_ld_n<KH>(cb + KP, y);
-      tmem_ld_wait();
-      tc_fence_before();
-#pragma unroll
-      for (int j = 0; j < KH; ++j) part[j] = x[j] + y[j];
+    constexpr uint32_t kXBytes = uint32_t(2 * kPcFrames * XS * sizeof(float));  // one CTA's partials
+    if (tid == 0) {
+      mbar_expect_tx(&bar_xfull, kXBytes);  // the peer's partials, before it may send them
+      mbar_arrive_remote(&bar_pfree, peer);  // our phase B is done: our slots may take them
     }
-    cluster_wait();
-    PC_MARK(9, 0);
     if (warp < kPcEpiWarps) {
+      // num (or den) partial = [q|r]_hi W_hi + [q|r]_lo W_hi (columns k) + [q|r]_hi W_lo (KP + k)
+      const uint32_t cb = tlane + S::C_DB + uint32_t(KH * hh);
+      tmem_ld_n<KH>(cb, part);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j0 = 0; j0 < KH; j0 += 4) {
+        float y[4];
+        tmem_ld<4>(cb + KP + j0, y);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 4; ++j) part[j0 + j] += y[j];
+      }
+      tc_fence_before();
       // lane m = 32q + lane of D_B: m < 64 -> num of frame m, else den of frame m - 64
       const int m = 32 * q + lane, nd = m >> 6, n = m & 63;
       float* dst = XB + ((int(rank) * 2 + nd) * kPcFrames + n) * XS + KH * hh;
-      const uint32_t rdst = dsmem_addr(dst, peer);
 #pragma unroll
-      for (int j = 0; j < KH; j += 4) {
-        const float4 v4 = make_float4(part[j], part[j + 1], part[j + 2], part[j + 3]);
-        *reinterpret_cast<float4*>(dst + j) = v4;
-        dsmem_st4(rdst + 4u * j, v4);
-      }
+      for (int j = 0; j < KH; j += 4)
+        *reinterpret_cast<float4*>(dst + j) = make_float4(part[j], part[j + 1], part[j + 2], part[j + 3]);
     }
-    cluster_arrive();
-    cluster_wait();
+    proxy_fence();  // the partials, for the bulk copy (async proxy)
+    __syncthreads();
+    if (tid == 0) {  // our partials -> the same place in the peer's slots, one bulk copy
+      mbar_wait_cluster(&bar_pfree, pass & 1);
+      PC_MARK(9, 0);
+      const float* src = XB + int(rank) * 2 * kPcFrames * XS;
+      asm volatile(
+          "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              dsmem_addr(src, peer)),
+          "r"(smem_addr(src)), "r"(kXBytes), "r"(dsmem_addr(&bar_xfull, peer))
+          : "memory");
+    }
+    PC_MARK(16, 0);
+    mbar_wait_cluster(&bar_xfull, pass & 1);
     PC_MARK(12, 0);
     // both CTAs: h of every frame, fixed order (own-rank-independent: rank 0 + rank 1 + tail)
     for (int it = tid; it < kPcFrames * (KP / 4); it += kPcThreads) {
-      const int n = it / (KP / 4), k4 = 4 * (it - n * (KP / 4));
+      // frame-fastest: a quarter warp touches 8 consecutive frames, conflict-free in both
+      // the exchange rows (stride XS) and the h core matrices
+      const int k4 = 4 * (it / kPcFrames), n = it % kPcFrames;
       const float4 a0 = *reinterpret_cast<const float4*>(XB + (0 * kPcFrames + n) * XS + k4);
       const float4 a1 = *reinterpret_cast<const float4*>(XB + (2 * kPcFrames + n) * XS + k4);
       const float4 b0 = *reinterpret_cast<const float4*>(XB + (1 * kPcFrames + n) * XS + k4);
@@ -685,9 +783,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPcThreads, 1) solve
       *reinterpret_cast<float4*>(Hh + o) = make_float4(hv[0], hv[1], hv[2], hv[3]);
       *reinterpret_cast<float4*>(Hl + o) = make_float4(tf32_lo(hv[0]), tf32_lo(hv[1]), tf32_lo(hv[2]), tf32_lo(hv[3]));
     }
+    PC_MARK(17, 0);
     proxy_fence();
     tc_fence_before();
     __syncthreads();
+    PC_MARK(18, 0);
   }
 
   PC_MARK(13, 0);
@@ -711,6 +811,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPcThreads, 1) solve
   cluster_arrive();  // no DSMEM access reaches an exited CTA
   cluster_wait();
   PC_MARK(15, 0);
+#ifdef ISNMF_PC_TRACE
+  if (g_pc_trace && blockIdx.x < 2 && (threadIdx.x & 31) == 0)
+    for (int i = 0; i < pc_n; ++i)
+      g_pc_trace[4096 + (blockIdx.x * 10 + (threadIdx.x >> 5)) * 512 + i] = pc_log[(threadIdx.x >> 5) * kPcLog + i];
+#endif
   if (warp == kPcIssueWarp) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
