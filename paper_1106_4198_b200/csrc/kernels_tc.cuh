@@ -42,6 +42,9 @@ constexpr int kPcFrames = 64;   // frames of a pair (phase-A N, half of phase-B 
 constexpr int kPcEpiWarps = 8;  // epilogue warps: (quarter q = warp & 3, frame half hh = warp >> 2)
 constexpr int kPcIssueWarp = 0; // its lane 0 also issues every MMA, between its epilogue steps
 constexpr int kPcTailWarp = 7;  // also the FP32 tail rows (quarter 3 waits for a slot first)
+// lane 0 of this warp issues phase A of tile 1 once tile 0's is done (quarter 2 waits for its
+// slot then; D_A[1] is its own accumulator, so the MMA issue order stays deterministic)
+constexpr int kPcA1Warp = 6;
 constexpr int kPcThreads = 256; // two warps per SM sub-partition: 255 registers, v + eps resident
 // chunk issue order within a tile: quarters 0, 1, 2, 3 (the issuing warp stages the first)
 __host__ __device__ constexpr int pc_chunk_quarter(int i) { return i & 3; }
@@ -554,11 +557,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPcThreads, 1) solve
       __syncthreads();
     }
     // ------------------------------------------------------------------ issuer (+ tail rows)
-    if (warp == kPcIssueWarp) {  // tile 0 now; tile 1 once the first chunk is queued
-      if (lane == 0) {
-        issue_phase_a(0);
-        if (stats_pass) issue_phase_a(1);
-      }
+    if (warp == kPcIssueWarp) {  // tile 0 now; tile 1 by warp kPcA1Warp once it is done
+      if (lane == 0) issue_phase_a(0);
       __syncwarp();
     }
     if (warp == kPcTailWarp && ntail > 0) {
@@ -575,11 +575,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPcThreads, 1) solve
       for (int t = 0; t < 2; ++t) {
         const int row = int(rank) * kPcRows + 128 * t + 32 * q + lane;
         const bool rowok = row < rowF;
+        const float rowmask = rowok ? 1.0f : 0.0f;
         const float* v = vr[t];
         PC_MARK(2, t);
         mbar_wait(&bar_a[t], pass & 1);
         PC_MARK(3, t);
         tc_fence_after();
+        if (t == 0 && warp == kPcA1Warp) {
+          if (lane == 0) issue_phase_a(1);
+          __syncwarp();
+        }
         const uint32_t cA = tlane + S::C_DA + uint32_t(64 * t + 32 * hh);
         if (!stats_pass) {
           // slot sl = c & 1 last held chunk c - 2 (or chunk c + 6 of the previous pass)
@@ -606,11 +611,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPcThreads, 1) solve
               float qv[4], rv[4];
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
-                const int j = 16 * hf + 4 * i + e, n = 32 * hh + j;
-                const bool valid = rowok && n < nf;
+                // rows past F must add nothing (rowmask 0); frames past nf only feed D_B rows
+                // that are never read (v = 0 there: finite values)
+                const int j = 16 * hf + 4 * i + e;
                 const float rr = rcp_approx(lam[4 * i + e] + eps);
-                qv[e] = valid ? v[j] * rr * rr : 0.0f;
-                rv[e] = valid ? rr : 0.0f;
+                rv[e] = rr * rowmask;
+                qv[e] = (v[j] * rv[e]) * rr;
               }
               const int mq = 32 * hh + 16 * hf + 4 * i;
               const int oq = pc_off_st(mq, lane), orr = pc_off_st(64 + mq, lane);
@@ -626,15 +632,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPcThreads, 1) solve
           mbar_arrive(&bar_full[c]);
           PC_MARK(6, c);
           if (warp == kPcIssueWarp) {  // the rest of the tile's chunks, in order
-            if (lane == 0) {
-              if (t == 0) {  // our chunk (the tile's first), then phase A of tile 1 behind it
-                issue_chunks(kPcIssueBefore, 1, pass);
-                issue_phase_a(1);
-                issue_chunks(kPcIssueBefore + 1, 3 - kPcIssueBefore, pass);
-              } else {
-                issue_chunks(4 + kPcIssueBefore, 4 - kPcIssueBefore, pass);
-              }
-            }
+            if (lane == 0) issue_chunks(4 * t + kPcIssueBefore, 4 - kPcIssueBefore, pass);
             __syncwarp();
           }
 
