@@ -712,7 +712,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPcThreads, 1) solve
       tc_fence_after();
     }
     PC_MARK(8, 0);
-    constexpr uint32_t kXBytes = uint32_t(2 * kPcFrames * XS * sizeof(float));  // one CTA's partials
+    // one CTA's partials: num and den rows of the nf frames (both CTAs of the pair have the same nf)
+    const uint32_t xrow_bytes = uint32_t(nf * XS * sizeof(float)), kXBytes = 2 * xrow_bytes;
     if (tid == 0) {
       mbar_expect_tx(&bar_xfull, kXBytes);  // the peer's partials, before it may send them
       mbar_arrive_remote(&bar_pfree, peer);  // our phase B is done: our slots may take them
@@ -740,24 +741,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPcThreads, 1) solve
     }
     proxy_fence();  // the partials, for the bulk copy (async proxy)
     __syncthreads();
-    if (tid == 0) {  // our partials -> the same place in the peer's slots, one bulk copy
+    if (tid == 0) {  // our partials -> the same place in the peer's slots (num rows, den rows)
       mbar_wait_cluster(&bar_pfree, pass & 1);
       PC_MARK(9, 0);
-      const float* src = XB + int(rank) * 2 * kPcFrames * XS;
-      asm volatile(
-          "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-              dsmem_addr(src, peer)),
-          "r"(smem_addr(src)), "r"(kXBytes), "r"(dsmem_addr(&bar_xfull, peer))
-          : "memory");
+      const uint32_t rbar = dsmem_addr(&bar_xfull, peer);
+#pragma unroll
+      for (int nd = 0; nd < 2; ++nd) {
+        const float* src = XB + (int(rank) * 2 + nd) * kPcFrames * XS;
+        asm volatile(
+            "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                dsmem_addr(src, peer)),
+            "r"(smem_addr(src)), "r"(xrow_bytes), "r"(rbar)
+            : "memory");
+      }
     }
     PC_MARK(16, 0);
     mbar_wait_cluster(&bar_xfull, pass & 1);
     PC_MARK(12, 0);
     // both CTAs: h of every frame, fixed order (own-rank-independent: rank 0 + rank 1 + tail)
-    for (int it = tid; it < kPcFrames * (KP / 4); it += kPcThreads) {
+    const int nk4 = (K + 3) >> 2;  // frames >= nf and atoms >= K keep h = 0
+    for (int it = tid; it < nf * nk4; it += kPcThreads) {
       // frame-fastest: a quarter warp touches 8 consecutive frames, conflict-free in both
       // the exchange rows (stride XS) and the h core matrices
-      const int k4 = 4 * (it / kPcFrames), n = it % kPcFrames;
+      const int k4 = 4 * (it / nf), n = it - (it / nf) * nf;
       const float4 a0 = *reinterpret_cast<const float4*>(XB + (0 * kPcFrames + n) * XS + k4);
       const float4 a1 = *reinterpret_cast<const float4*>(XB + (2 * kPcFrames + n) * XS + k4);
       const float4 b0 = *reinterpret_cast<const float4*>(XB + (1 * kPcFrames + n) * XS + k4);
