@@ -158,6 +158,36 @@ def dist_done(world):
 MMA_3XTF32_PEAK = 1020.0 / 3 * 148 * 1.965e9 / 1e12
 
 
+def measured_peaks():
+    try:
+        return json.load(open(MEASURED))
+    except (OSError, ValueError):
+        return {}
+
+
+def tcgen05_3xtf32_peak():
+    """Useful-product ceiling of 3xTF32 on the 5th-generation tensor cores: the dense tf32
+    rate is half the bf16 rate, taken from the MEASURED bf16 burst figure in
+    MEASURED_PEAKS.json (else the nominal 2.25 PFLOP/s of B200_PROFILING.md), and every
+    useful product costs three tf32 products (hi*hi + hi*lo + lo*hi)."""
+    mp = measured_peaks()
+    bf16 = mp.get("bf16_tflops")
+    src = ("MEASURED_PEAKS.json bf16_tflops %.1f (burst) / 2 (tf32) / 3 (3xTF32)" % bf16 if bf16 else
+           "fallback: nominal 2250 TFLOP/s bf16 dense (B200_PROFILING.md) / 2 / 3")
+    return (bf16 or 2250.0) / 2.0 / 3.0, src
+
+
+KERNELS = {
+    "K1C": "solve_pair_kernel (K1C: 2-CTA cluster per 56 frames, tcgen05.mma kind::tf32 3xTF32 with TMEM "
+           "accumulators and the dictionary rows as TMEM A operand, TMA bulk loads, DSMEM partial exchange)",
+    "K1M": "solve_mma_kernel (K1M: 3xTF32 mma.sync for every contraction)",
+    "K1": "solve_kernel (FP32 FMA + 3xTF32 mma.sync phase A)",
+    "K1T": "solve_large_tc_kernel (K1T: tcgen05 phase B, mma.sync phase A)",
+    "K1L": "solve_large_kernel (3xTF32 mma.sync)",
+    "generic": "solve_generic_kernel (FP32)",
+}
+
+
 def k1_traffic(config):
     """DRAM bytes per K1 launch of this config from its committed ncu --set full
     capture (profiles/k1_traffic_<config>.json), or None when there is none."""
@@ -309,13 +339,18 @@ def run_batch(args, rank, world):
                                                  f"U(0.1,1); V device-resident, device-timed (CUDA events)",
                                      "parallelism": "replicas" if world > 1 else "single",
                                      "l2": "inputs larger than L2 (V = %.2f GB fp32)" % (N * F * 4 / 1e9)},
-                          "roofline": {"bound": "fp32", "achieved": flops / t / 1e12, "peak": peak,
-                                       "unit": "TFLOP/s", "frac": flops / t / 1e12 / peak,
+                          "roofline": {"bound": "tensor", "achieved": flops / t / 1e12, "peak": MMA_3XTF32_PEAK,
+                                       "unit": "TFLOP/s", "frac": flops / t / 1e12 / MMA_3XTF32_PEAK,
+                                       "kernel": "solve_mma_kernel multi-tile (K1M: 3xTF32 mma.sync) + fold_commit",
                                        "flops_per_step": flops,
                                        "flop_model": "12FKN per epoch (H pass 6FKN + statistics 6FKN; the "
                                                      "objective shares the next epoch's first W h) + 2FKN",
                                        "traffic": None,
-                                       "peak_source": "nominal FP32 FMA peak 148 SM x 128 x 2 x 1.965 GHz"},
+                                       "peak_source": "mma.sync m16n8k8 tf32 1020 flop/clk/SM (tools/probe/mma_probe2.cu)"
+                                                      " / 3 (3xTF32), 148 SM x 1.965 GHz",
+                                       "fp32_roofline": {"peak": peak, "frac": flops / t / 1e12 / peak,
+                                                         "note": "north_star: FP32 FMA peak, nominal 148 SM x 128 x 2 "
+                                                                 "x 1.965 GHz; target >= 50%"}},
                           "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clk.summary(),
                           "final_obj": float(out["obj"][-1]), "initial_obj": out["initial_obj"]}), flush=True)
 
@@ -520,6 +555,30 @@ def run_engine(args, rank, world):
     compare = None
     if rank == 0 and args.config == "c3" and not args.no_compare:
         compare = batch_vs_online()
+    solver = eng.solver()
+    if solver in ("K1C", "K1T"):  # tcgen05: the 3xTF32 useful-product ceiling of the tensor cores
+        tpeak, tsrc = tcgen05_3xtf32_peak()
+    else:  # legacy mma.sync pipe
+        tpeak = MMA_3XTF32_PEAK
+        tsrc = "mma.sync m16n8k8 tf32 1020 flop/clk/SM (tools/probe/mma_probe2.cu) / 3 (3xTF32), 148 SM x 1.965 GHz"
+    pass_tflops = flops_per_frame * N * args.steps / (ms_total / 1e3) / 1e12
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": tpeak, "unit": "TFLOP/s", "frac": achieved / tpeak,
+                "peak_source": tsrc,
+                "kernel": KERNELS.get(solver, solver), "solver": solver,
+                "flop_model": "6*F*K*(I+1) useful flops per frame (I MM iterations of Lam = W h, W^T q, W^T r "
+                              "plus the statistics pass), fp32-equivalent; the 3xTF32 split products are not counted",
+                "flops_per_launch": flops_per_frame * frames_per_launch, "ms_per_launch": k1_ms,
+                "traffic": traffic, "traffic_source": traffic_src,
+                "traffic_unit": "bytes per launch (ncu dram__bytes_read+write)",
+                "algorithmic_bytes_per_launch": frames_per_launch * (4 * F + 16 * K),
+                "algorithmic_bytes_note": "per frame: V read once (4F) + the fp64 warm activation read and written (16K)",
+                "fp32_roofline": {"peak": peak, "achieved": achieved, "frac": achieved / peak,
+                                  "pass_frac": pass_tflops / peak,
+                                  "note": "north_star roofline: the pass's flops at the FP32 FMA peak (nominal 148 SM "
+                                          "x 128 x 2 x 1.965 GHz = 74.4 TFLOP/s; MEASURED_PEAKS.json has no FP32 "
+                                          "entry, tools/probe measured 72.4 on this pool); target >= 50%"},
+                "k1_share_of_step": kstats["solve_ms"] / kstats["span_ms"],
+                "k2_us_per_minibatch": 1e3 * k2_ms}
     if rank == 0:
         metric = ("online IS-NMF frames/sec (F=513,K=50,beta=4096)" if args.config == "c3" else
                   f"online IS-NMF frames/sec ({args.config}: F={F},K={K},beta={beta})")
@@ -532,28 +591,7 @@ def run_engine(args, rank, world):
                                        f"warm store h0=1 (state re-initialised outside the timed region)",
                            "global_batch": beta, "parallelism": "replicas" if world > 1 else "single",
                            "l2": "inputs larger than L2 (V = %.2f GB fp32)" % (N * F * 4 / 1e9)},
-                "roofline": {"bound": "fp32", "bound_note": "north_star roofline: the pass's flops at the FP32 FMA "
-                                                    "peak (compute bound, ~690 flop/B); K1M computes on the HMMA "
-                                                    "pipe, whose 3xTF32 ceiling is tensor_pipe_peak",
-                             "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                             "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
-                             "traffic_unit": "bytes per launch (ncu dram__bytes_read+write)",
-                             "algorithmic_bytes_per_launch": frames_per_launch * (4 * F + 16 * K),
-                             "algorithmic_bytes_note": "per frame: V read once (4F) + the fp64 warm activation read and written (16K)",
-                             "kernel": ("solve_mma_kernel (K1M: 3xTF32 mma.sync for every contraction)"
-                                        if K <= 56 and os.environ.get("ISNMF_MMA", "1") != "0" else
-                                        "solve_kernel (FP32 FMA + 3xTF32 mma.sync phase A)" if K <= 64 else
-                                        "solve_large_tc_kernel / solve_large_kernel (tcgen05 / mma.sync)"),
-                             "tensor_pipe_frac": achieved / MMA_3XTF32_PEAK,
-                             "tensor_pipe_peak": MMA_3XTF32_PEAK,
-                             "ms_per_launch": k1_ms,
-                             "flops_per_launch": flops_per_frame * frames_per_launch,
-                             "k1_share_of_step": kstats["solve_ms"] / kstats["span_ms"],
-                             "k2_us_per_minibatch": 1e3 * k2_ms,
-                             "pass_frac": flops_per_frame * N * args.steps / (ms_total / 1e3) / 1e12 / peak,
-                             "peak_source": "nominal FP32 FMA peak 148 SM x 128 x 2 x 1.965 GHz = 74.4 TFLOP/s "
-                                            "(MEASURED_PEAKS.json has no FP32 entry; tools/probe measured 72.4 "
-                                            "on this pool)"},
+                "roofline": roofline,
                 "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches, "batch_vs_online": compare,
                 "clocks": clk.summary(), "wall_s": wall,
                 "final": {"t": st["t"], "commits": st["commits"], "last_minibatch_obj": st["last_minibatch_obj"]}}
