@@ -229,9 +229,13 @@ static __device__ unsigned long long* g_pc_trace = nullptr;  // (tc_table.cu's c
 // barrier.cluster.arrive.release would be waited for), dumped at the end of the launch to
 // g_pc_trace[4096 + (cta * 10 + warp) * 512 ..]: clock64 << 16 | site << 8 | (arg & 0xff)
 constexpr int kPcLog = 96;
+#ifndef ISNMF_PC_TRACE_MIN
+#define ISNMF_PC_TRACE_MIN 0  // 7: pass-level sites only (the whole launch fits the log)
+#endif
 #define PC_MARK(site, arg)                                                                            \
   do {                                                                                                \
-    if ((threadIdx.x & 31) == 0 && pc_n < kPcLog)                                                     \
+    if ((threadIdx.x & 31) == 0 && pc_n < kPcLog &&                                                   \
+        ((site) >= ISNMF_PC_TRACE_MIN && !((site) >= 21 && (site) <= 25) || ISNMF_PC_TRACE_MIN == 0))   \
       pc_log[(threadIdx.x >> 5) * kPcLog + pc_n++] =                                                  \
           (unsigned long long)clock64() << 16 | (unsigned long long)(site) << 8 | ((arg) & 0xff);     \
   } while (0)
@@ -284,7 +288,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPcThreads, 1) solve
   __shared__ unsigned long long pc_log[(kPcThreads / 32) * kPcLog];
 #endif
 
-  pdl_wait();
+  PC_MARK(19, 0);
+  // ---- before the PDL wait (overlaps the previous mini-batch's K2): nothing K2 writes
   if (warp == kPcIssueWarp) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&s_tmem)),
                  "r"(512));
@@ -293,7 +298,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPcThreads, 1) solve
   cluster_arrive();  // (waited before the first access to the peer's shared memory)
   if (tid == 0) {
     s_bad = 0;
-    s_go = !(*a.status || (a.halt && *a.halt));
     mbar_init(&bar_w, 1);
     for (int i = 0; i < 2; ++i) mbar_init(&bar_a[i], 1);
     for (int i = 0; i < 8; ++i) {
@@ -306,6 +310,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPcThreads, 1) solve
     mbar_init(&bar_pfree, 1);
     mbar_init(&bar_xfull, 1);  // thread 0's arrive.expect_tx + the peer's bulk copy
     asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  if (tid < kPcFrames) {
+    const int64_t fr = tid < nf ? (a.vsel ? a.vsel[n0 + tid] : a.v0 + n0 + tid) : 0;
+    fptr[tid] = a.V + fr * a.ldv;
+  }
+  __syncthreads();
+  const int q = warp & 3, hh = (warp >> 2) & 1;
+  // v + eps of this thread's cells (rows 128t + 32q + lane, frames 32hh ..), resident for every pass
+  float vr[2][32];
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    const int row = int(rank) * kPcRows + 128 * t + 32 * q + lane;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int n = 32 * hh + j;
+      vr[t][j] = (row < rowF && n < nf ? __ldg(fptr[n] + row) : 0.0f) + eps;
+    }
+  }
+  pdl_wait();
+  PC_MARK(20, 0);
+  if (tid == 0) {
+    s_go = !(*a.status || (a.halt && *a.halt));
     if (s_go) {  // this CTA's half of W^T by TMA bulk copies
       const uint32_t bytes = uint32_t(S::WB_FLOATS) * 4u;
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&bar_w)), "r"(bytes));
@@ -321,14 +347,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPcThreads, 1) solve
       }
     }
   }
-  if (tid < kPcFrames) {
-    const int64_t fr = tid < nf ? (a.vsel ? a.vsel[n0 + tid] : a.v0 + n0 + tid) : 0;
-    fptr[tid] = a.V + fr * a.ldv;
-    if (a.h0_mode == 1 && tid < nf) {
-      const int64_t col = warm_col(a, n0 + tid);
-      colv[tid] = col;
-      tagv[tid] = a.T[col];
-    }
+  // the dictionary rows for TMEM (W_A: warp (q, t = hh) holds rows 128t + 32q + lane), loaded
+  // now, stored after the warm-store reads below are in flight
+  const int wa_row = int(rank) * kPcRows + 128 * hh + 32 * q + lane;
+  float4 wa[KP / 4];
+#pragma unroll
+  for (int k4 = 0; k4 < KP / 4; ++k4)
+    wa[k4] = wa_row < rowF ? __ldg(reinterpret_cast<const float4*>(a.W32 + size_t(wa_row) * a.ws + 4 * k4))
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+  PC_MARK(26, 0);
+  if (a.h0_mode == 1 && tid < nf) {  // warm-store column and tag of every frame
+    const int64_t col = warm_col(a, n0 + tid);
+    colv[tid] = col;
+    tagv[tid] = a.T[col];
   }
   __syncthreads();
   if (a.h0_mode == 2) {  // fresh: mean of each frame (fresh_h_init's v.mean())
@@ -340,56 +371,91 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPcThreads, 1) solve
     }
     __syncthreads();
   }
+  PC_MARK(27, 0);
   // h0 of every frame of the pair (both CTAs hold all of h), zero outside n < nf, k < K
-  for (int idx = tid; idx < kPcFrames * KP; idx += kPcThreads) {
-    const int n = idx / KP, k = idx - n * KP;
-    float val = 0.0f;
-    if (n < nf && k < K) {
-      int bad = 0;
-      val = solve_h0(a, n0 + n, k, a.h0_mode == 1 ? colv[n] : 0, a.h0_mode == 1 ? tagv[n] : 0u,
-                     a.h0_mode == 2 ? meanv[n] : 0.0, bad);
-      if (a.check_h0 && bad) s_bad = 1;
+  if (a.h0_mode == 1 && kPcThreads == 4 * kPcFrames) {
+    // warm store (kernels.cuh warm_value / solve_h0): thread (frame n, k phase kq) issues all its
+    // U and P loads before using any (the store is cold in HBM: one latency, not KP / 4)
+    constexpr int NKQ = (KP + 3) / 4;
+    const int n = tid >> 2, kq = tid & 3;
+    const bool fr = n < nf;
+    const int64_t col = fr ? colv[n] : 0;
+    const uint32_t tag = fr ? tagv[n] : 0u;
+    const double* urow = a.U + size_t(col) * K;
+    const double* prow = a.P + size_t(tag) * K;
+    const double* pnow = a.P + size_t(a.c_now) * K;
+    double u[NKQ], pt[NKQ], pn[NKQ];
+#pragma unroll
+    for (int j = 0; j < NKQ; ++j) {
+      const int k = 4 * j + kq;
+      const bool ok = fr && k < K;
+      u[j] = ok ? urow[k] : 0.0;
+      pt[j] = ok ? prow[k] : 1.0;
+      pn[j] = ok ? pnow[k] : 1.0;
     }
-    Hh[pc_off_h<KP>(n, k)] = val;
-    Hl[pc_off_h<KP>(n, k)] = tf32_lo(val);
+    int bad = 0;
+#pragma unroll
+    for (int j = 0; j < NKQ; ++j) {
+      const int k = 4 * j + kq;
+      if (k >= KP) continue;
+      float val = 0.0f;
+      if (fr && k < K) {
+        const double h0 = u[j] * (pn[j] / pt[j]);
+        if (!(h0 > 0.0)) bad = 1;
+        val = h0 < double(kWarmFloor) && h0 > 0.0 ? kWarmFloor : float(h0);
+      }
+      Hh[pc_off_h<KP>(n, k)] = val;
+      Hl[pc_off_h<KP>(n, k)] = tf32_lo(val);
+    }
+    if (a.check_h0 && bad) s_bad = 1;
+  } else {
+    for (int idx = tid; idx < kPcFrames * KP; idx += kPcThreads) {
+      const int n = idx / KP, k = idx - n * KP;
+      float val = 0.0f;
+      if (n < nf && k < K) {
+        int bad = 0;
+        val = solve_h0(a, n0 + n, k, a.h0_mode == 1 ? colv[n] : 0, a.h0_mode == 1 ? tagv[n] : 0u,
+                       a.h0_mode == 2 ? meanv[n] : 0.0, bad);
+        if (a.check_h0 && bad) s_bad = 1;
+      }
+      Hh[pc_off_h<KP>(n, k)] = val;
+      Hl[pc_off_h<KP>(n, k)] = tf32_lo(val);
+    }
   }
+  PC_MARK(28, 0);
   // tail rows of W (rows >= 512) for the FP32 tail warp
   for (int idx = tid; idx < ntail * KP; idx += kPcThreads) {
     const int i = idx / KP, k = idx - i * KP;
     Wt[idx] = k < K ? a.W32[size_t(2 * kPcRows + i) * a.ws + k] : 0.0f;
   }
-  __syncthreads();
   const uint32_t tmem = s_tmem;
-  // dictionary rows -> TMEM (W_A): warp (q, hh) writes tile hh, lanes 32q.. = rows 128hh + 32q + lane
-  if (warp < kPcEpiWarps && s_go) {
-    const int q = warp & 3, t = warp >> 2;
-    const int row = int(rank) * kPcRows + 128 * t + 32 * q + lane;
+  {  // W_A: hi = the fp32 value (the tensor core reads its tf32 part), lo = the remainder
     float hi[KP], lo[KP];
-    const float* wr = a.W32 + size_t(row) * a.ws;
 #pragma unroll
     for (int k4 = 0; k4 < KP / 4; ++k4) {
-      const float4 w = row < rowF ? __ldg(reinterpret_cast<const float4*>(wr + 4 * k4)) : make_float4(0.f, 0.f, 0.f, 0.f);
-      hi[4 * k4] = w.x;
-      hi[4 * k4 + 1] = w.y;
-      hi[4 * k4 + 2] = w.z;
-      hi[4 * k4 + 3] = w.w;
+      hi[4 * k4] = wa[k4].x;
+      hi[4 * k4 + 1] = wa[k4].y;
+      hi[4 * k4 + 2] = wa[k4].z;
+      hi[4 * k4 + 3] = wa[k4].w;
     }
 #pragma unroll
     for (int k = 0; k < KP; ++k) {
       if (k >= K) hi[k] = 0.0f;
       lo[k] = tf32_lo(hi[k]);
     }
-    const uint32_t ta = tmem + (uint32_t(32 * q) << 16) + uint32_t(t * KP2);
+    const uint32_t ta = tmem + (uint32_t(32 * q) << 16) + uint32_t(hh * KP2);
     tmem_st_n<KP>(ta, hi);
     tmem_st_n<KP>(ta + KP, lo);
     tmem_st_wait();
   }
+  PC_MARK(29, 0);
   proxy_fence();
   tc_fence_before();
   // the go decision of both CTAs (a status bit set by another cluster of this launch could
   // otherwise split the pair); also orders every prologue read of the warm store before the
   // owners' final writes
   cluster_wait();  // the peer has started: its shared memory may be accessed
+  PC_MARK(30, 0);
   if (tid == 0) {
     const uint32_t ra = dsmem_addr(&s_go_peer, peer);
     asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(ra), "r"(s_go) : "memory");
@@ -410,7 +476,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPcThreads, 1) solve
   mbar_wait(&bar_w, 0);
   PC_MARK(1, 0);
 
-  const int q = warp & 3, hh = (warp >> 2) & 1;
   const uint32_t tlane = tmem + (uint32_t(32 * q) << 16);
   float divacc = 0.0f;
   // ---- MMA issue (lane 0 of warp kPcIssueWarp, in program order between its epilogue steps)
@@ -517,27 +582,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPcThreads, 1) solve
     }
   };
 
-  // v + eps of this thread's cells (rows 128t + 32q + lane, frames 32hh ..), resident for every pass
-  float vr[2][32];
-  if (warp < kPcEpiWarps) {
-#pragma unroll
-    for (int t = 0; t < 2; ++t) {
-      const int row = int(rank) * kPcRows + 128 * t + 32 * q + lane;
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const int n = 32 * hh + j;
-        vr[t][j] = (row < rowF && n < nf ? __ldg(fptr[n] + row) : 0.0f) + eps;
-      }
-    }
-  }
   const int passes = a.iters + 1;
   for (int pass = 0; pass < passes; ++pass) {
     const bool stats_pass = pass == a.iters;
     pass_no = pass;
+    if (stats_pass) pdl_trigger();
+    // ------------------------------------------------------------------ issuer (+ tail rows)
+    if (warp == kPcIssueWarp) {  // tile 0 now; tile 1 by warp kPcA1Warp once it is done
+      if (lane == 0) issue_phase_a(0);
+      __syncwarp();
+    }
+    if (warp == kPcTailWarp && ntail > 0) {
+      tail_rows(lane, 32, stats_pass);
+      if (stats_pass && rank == 1 && a.stats) {
+        __syncwarp();
+        tail_stats(lane, 32);
+      }
+      __syncwarp();
+    }
     if (stats_pass) {
-      pdl_trigger();
-      // h^T (hi | lo rows) for the statistics B operand; the slots are free (the last
-      // update has read the exchange buffer before the end-of-pass barrier)
+      // h^T (hi | lo rows) for the statistics B operand, built while phase A runs; the slots are
+      // free (the last update read the exchange buffer before the end-of-pass barrier)
       for (int idx = tid; idx < S::HT_ROWS * (kPcFrames / 4); idx += kPcThreads) {
         const int kp = idx / (kPcFrames / 4), n4 = 4 * (idx - kp * (kPcFrames / 4));
         float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -555,19 +620,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPcThreads, 1) solve
       }
       proxy_fence();
       __syncthreads();
-    }
-    // ------------------------------------------------------------------ issuer (+ tail rows)
-    if (warp == kPcIssueWarp) {  // tile 0 now; tile 1 by warp kPcA1Warp once it is done
-      if (lane == 0) issue_phase_a(0);
-      __syncwarp();
-    }
-    if (warp == kPcTailWarp && ntail > 0) {
-      tail_rows(lane, 32, stats_pass);
-      if (stats_pass && rank == 1 && a.stats) {
-        __syncwarp();
-        tail_stats(lane, 32);
-      }
-      __syncwarp();
+      PC_MARK(31, 0);
     }
     // ------------------------------------------------------------------ epilogue warps
     if (warp < kPcEpiWarps) {
@@ -640,10 +693,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPcThreads, 1) solve
           // statistics pass: q / r (hi | lo) of this tile into TMEM as the A operands (A_S
           // overlays W_A: both tiles' phase-A MMAs must be done; for tile 1 the tile-0
           // statistics MMAs are, since their D_S was drained below first)
+          PC_MARK(32, t);
           if (t == 0) {
             mbar_wait(&bar_a[1], pass & 1);
             tc_fence_after();
           }
+          PC_MARK(33, t);
 #pragma unroll
           for (int hf = 0; hf < 2; ++hf) {
             float lam[16], x[16];
@@ -691,11 +746,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPcThreads, 1) solve
             tmem_ld_n<KH>(tlane + S::C_DS + uint32_t(64 * ab + KH * hh), sv);
             tmem_ld_wait();
             if (out && rowok) {
+              float* o = out + size_t(ab) * FP * KP + size_t(KH * hh) * FP + row;
+              const int kend = min(KH, K - KH * hh);
 #pragma unroll
-              for (int j = 0; j < KH; ++j) {
-                const int k = KH * hh + j;
-                if (k < K) out[size_t(ab) * FP * KP + size_t(k) * FP + row] = sv[j];
-              }
+              for (int j = 0; j < KH; ++j, o += FP)
+                if (j < kend) *o = sv[j];
             }
           }
           tc_fence_before();
@@ -808,7 +863,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPcThreads, 1) solve
   }
   // final h of the frames this CTA owns (rank r: frames 32r ..)
   const int own0 = 32 * int(rank), nown = max(0, min(32, nf - own0));
-  write_final_h(a, n0 + own0, nown, [&](int n, int k) { return Hh[pc_off_h<KP>(own0 + n, k)]; });
+  if (a.h0_mode == 1 && a.write_store) {
+    // warm store (kernels.cuh warm_put): thread (frame own0 + tid / 8, k = tid % 8 + 8 j) issues every
+    // U / P load of its cells before any store (one HBM latency instead of one per cell)
+    constexpr int NJ = KP / 8;
+    const int nl = tid >> 3, k0 = tid & 7, n = own0 + nl;
+    const bool fr = nl < nown;
+    const int64_t col = fr ? colv[n] : 0;
+    const uint32_t tag = fr ? tagv[n] : 0u;
+    const double* urow = a.U + size_t(col) * K;
+    const double* prow = a.P + size_t(tag) * K;
+    const double* pnow = a.P + size_t(a.c_now) * K;
+    double u[NJ], pt[NJ], pn[NJ];
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      const int k = k0 + 8 * j;
+      const bool ok = fr && k < K;
+      u[j] = ok ? urow[k] : 0.0;
+      pt[j] = ok ? prow[k] : 1.0;
+      pn[j] = ok ? pnow[k] : 1.0;
+    }
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      const int k = k0 + 8 * j;
+      if (!fr || k >= K) continue;
+      const float h = Hh[pc_off_h<KP>(n, k)];
+      const double h0 = u[j] * (pn[j] / pt[j]);
+      a.U[size_t(col) * K + k] = h0 < double(kWarmFloor) ? h0 * (double(h) / double(kWarmFloor)) : double(h);
+      if (a.Hout) a.Hout[size_t(n0 + n) * K + k] = h;
+    }
+    __syncthreads();  // every U write of this CTA has used its column's old tag
+    if (tid < nown) a.T[colv[own0 + tid]] = a.c_now;
+  } else {
+    write_final_h(a, n0 + own0, nown, [&](int n, int k) { return Hh[pc_off_h<KP>(own0 + n, k)]; });
+  }
   tc_fence_before();
   __syncthreads();
   PC_MARK(14, 0);
