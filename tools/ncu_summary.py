@@ -14,8 +14,8 @@ def ncu(*args):
     return subprocess.run(["ncu", "-i", rep, *args], capture_output=True, text=True).stdout
 
 
-raw = list(csv.reader(io.StringIO(ncu("--page", "raw", "--csv"))))
-h, v = raw[0], raw[2]
+raw = list(csv.reader(io.StringIO(ncu("--page", "raw", "--csv", "--print-units", "base"))))
+h, u, v = raw[0], raw[1], raw[2]
 want = ["gpu__time_duration.sum", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
         "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
         "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
@@ -26,10 +26,12 @@ want = ["gpu__time_duration.sum", "sm__throughput.avg.pct_of_peak_sustained_elap
         "sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_active",
         "sm__inst_executed_pipe_tensor_subpipe_hmma.avg.pct_of_peak_sustained_active",
         "sm__ops_path_tensor_src_tf32_dst_fp32.avg.pct_of_peak_sustained_elapsed",
-        "sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active"]
+        "sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+        "sm__inst_executed_pipe_tc.avg.pct_of_peak_sustained_active"]
 for w in want:
     if w in h:
-        print(f"{w:70s} {v[h.index(w)]}")
+        print(f"{w:70s} {v[h.index(w)]} {u[h.index(w)]}")
 st = {n.replace("smsp__pcsamp_warps_issue_stalled_", ""): int(float(v[i].replace(",", "") or 0))
       for i, n in enumerate(h) if n.startswith("smsp__pcsamp_warps_issue_stalled_") and not n.endswith("not_issued")}
 tot = sum(st.values())
