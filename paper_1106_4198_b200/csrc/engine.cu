@@ -825,7 +825,12 @@ int online_enqueue(isnmf_online* c, const float* frames, int64_t ldv, int64_t n,
   double ramp = double(c->beta);
   while (pos < n_eff) {
     const int64_t rb = std::max<int64_t>(int64_t(c->beta), int64_t(ramp / c->beta) * c->beta);
-    const int64_t cf = std::min<int64_t>(std::min<int64_t>(c->chunk, rb), n_eff - pos);
+    // ... and shrink towards the end (at most a quarter of what is left, whole mini-batches):
+    // the last chunk's compute (copy-bound shapes) or copy (compute-bound ones) is not
+    // overlapped, so it must be short — a 64-mini-batch last chunk cost 8 ms per config-3 pass
+    const int64_t rem = n_eff - pos;
+    const int64_t tail = std::max<int64_t>(int64_t(c->beta), (rem / 4) / c->beta * c->beta);
+    const int64_t cf = std::min<int64_t>(std::min<int64_t>(std::min<int64_t>(c->chunk, rb), tail), rem);
     ramp *= ramp_factor(c->K, c->iters);
     CU(cudaStreamWaitEvent(c->xs, c->ev_free[buf], 0));
     if (ldv == c->F)  // contiguous frames: one linear DMA (2D copies run far below PCIe speed)

@@ -40,16 +40,18 @@ namespace isnmf_dev {
 constexpr int kPcRows = 256;    // dictionary rows per CTA
 constexpr int kPcFrames = 64;   // frames of a pair (phase-A N, half of phase-B M)
 constexpr int kPcEpiWarps = 8;  // epilogue warps: (quarter q = warp & 3, frame half hh = warp >> 2)
-constexpr int kPcIssueWarp = 0; // its lane 0 also issues every MMA, between its epilogue steps
+constexpr int kPcIssueWarp = 0; // its lane 0 issues phase A, tile 0's chunks and the statistics MMAs
 constexpr int kPcTailWarp = 7;  // also the FP32 tail rows (quarter 3 waits for a slot first)
 // lane 0 of this warp issues phase A of tile 1 once tile 0's is done (quarter 2 waits for its
 // slot then; D_A[1] is its own accumulator, so the MMA issue order stays deterministic)
 constexpr int kPcA1Warp = 6;
 constexpr int kPcThreads = 256; // two warps per SM sub-partition: 255 registers, v + eps resident
-// chunk issue order within a tile: quarters 0, 1, 2, 3 (the issuing warp stages the first)
-__host__ __device__ constexpr int pc_chunk_quarter(int i) { return i & 3; }
-__host__ __device__ constexpr int pc_quarter_chunk(int q) { return q & 3; }
-constexpr int kPcIssueBefore = 0;  // chunks of a tile the issuer issues before staging its own
+// chunk issue order within tile t: quarters t, t + 1, t + 2, t + 3 (mod 4).  Tile t's chunks
+// are issued by lane 0 of warp t (quarter t, frames 0..31), right after it has staged the
+// tile's first chunk; warp 1 takes over from warp 0 at the tile boundary (mbarrier handoff +
+// tcgen05 fences keep the issue order), so warp 0 stages its tile-1 chunk while warp 1 issues
+__host__ __device__ constexpr int pc_chunk_quarter(int t, int i) { return (i + t) & 3; }
+__host__ __device__ constexpr int pc_quarter_chunk(int t, int q) { return (q - t) & 3; }
 constexpr int kPcMaxTail = 8;   // rows >= 512 on the FP32 pipe
 constexpr int kPcSlotFloats = 2 * 128 * 32;
 
@@ -271,6 +273,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPcThreads, 1) solve
   // exchange: bar_pfree = the peer's phase B is done (its slots take our partials), bar_xfull =
   // the peer's partials have landed in our slots (bulk copy, complete_tx)
   __shared__ __align__(8) uint64_t bar_pfree, bar_xfull;
+  __shared__ __align__(8) uint64_t bar_hand;  // tile 0's chunks are issued (warp 0 -> warp 1)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t rank = cluster_ctarank(), peer = rank ^ 1u;
@@ -309,6 +312,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPcThreads, 1) solve
     mbar_init(&bar_s, 1);
     mbar_init(&bar_pfree, 1);
     mbar_init(&bar_xfull, 1);  // thread 0's arrive.expect_tx + the peer's bulk copy
+    mbar_init(&bar_hand, 1);
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   if (tid < kPcFrames) {
@@ -500,7 +504,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPcThreads, 1) solve
     constexpr uint32_t id1 = umma_idesc_tf32(128, KP2, 1, 0), id2 = umma_idesc_tf32(128, NHI, 1, 0);
 #pragma unroll 1
     for (int c = c0; c < c0 + n; ++c) {
-      const int sl = c & 1, t = c >> 2, qq = pc_chunk_quarter(c & 3);
+      const int sl = c & 1, t = c >> 2, qq = pc_chunk_quarter(t, c & 3);
+      if (c == 4) {  // tile 0's MMAs were issued by warp 0
+        mbar_wait(&bar_hand, pass & 1);
+        tc_fence_after();
+      }
       PC_MARK(21, c);
       mbar_wait(&bar_full[c], pass & 1);
       PC_MARK(22, c);
@@ -517,6 +525,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPcThreads, 1) solve
         umma_tf32(tmem + S::C_DB, a1, bw, id2, 1u);
       }
       umma_commit(&bar_empty[c]);
+      if (c == 3) {
+        tc_fence_before();
+        mbar_arrive(&bar_hand);
+      }
     }
     if (c0 + n == 8) {
       umma_commit(&bar_b);
@@ -641,11 +653,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPcThreads, 1) solve
         const uint32_t cA = tlane + S::C_DA + uint32_t(64 * t + 32 * hh);
         if (!stats_pass) {
           // slot sl = c & 1 last held chunk c - 2 (or chunk c + 6 of the previous pass)
-          const int c = 4 * t + pc_quarter_chunk(q), sl = c & 1;
-          if (kPcIssueBefore > 0 && warp == kPcIssueWarp) {  // chunks ahead of our own
-            if (lane == 0) issue_chunks(4 * t, kPcIssueBefore, pass);
-            __syncwarp();
-          }
+          const int c = 4 * t + pc_quarter_chunk(t, q), sl = c & 1;
           PC_MARK(4, c);
           if (c >= 2)
             mbar_wait(&bar_empty[c - 2], pass & 1);
@@ -684,8 +692,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPcThreads, 1) solve
           proxy_fence();
           mbar_arrive(&bar_full[c]);
           PC_MARK(6, c);
-          if (warp == kPcIssueWarp) {  // the rest of the tile's chunks, in order
-            if (lane == 0) issue_chunks(4 * t + kPcIssueBefore, 4 - kPcIssueBefore, pass);
+          if (warp == t) {  // this tile's chunks, in order (ours first)
+            if (lane == 0) issue_chunks(4 * t, 4, pass);
             __syncwarp();
           }
 
@@ -760,35 +768,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPcThreads, 1) solve
     if (stats_pass) break;
     // ------------------------------------------------------------------ h update
     // all warps: D_B -> this CTA's num / den partials -> exchange -> h *= sqrt(num / den)
-    float part[KH];
     PC_MARK(7, 0);
-    if (warp < kPcEpiWarps) {
-      mbar_wait(&bar_b, pass & 1);
-      tc_fence_after();
-    }
+    mbar_wait(&bar_b, pass & 1);  // (every warp is an epilogue warp)
+    tc_fence_after();
     PC_MARK(8, 0);
-    // one CTA's partials: num and den rows of the nf frames (both CTAs of the pair have the same nf)
-    const uint32_t xrow_bytes = uint32_t(nf * XS * sizeof(float)), kXBytes = 2 * xrow_bytes;
     if (tid == 0) {
-      mbar_expect_tx(&bar_xfull, kXBytes);  // the peer's partials, before it may send them
+      mbar_expect_tx(&bar_xfull, uint32_t(2 * nf * XS * sizeof(float)));  // the peer's partials, before it may send them
       mbar_arrive_remote(&bar_pfree, peer);  // our phase B is done: our slots may take them
     }
-    if (warp < kPcEpiWarps) {
+    {
+      // lane m = 32q + lane of D_B: m < 64 -> num of frame m, else den of frame m - 64;
       // num (or den) partial = [q|r]_hi W_hi + [q|r]_lo W_hi (columns k) + [q|r]_hi W_lo (KP + k)
+      const int m = 32 * q + lane, nd = m >> 6, n = m & 63;
+      float part[KH];
       const uint32_t cb = tlane + S::C_DB + uint32_t(KH * hh);
       tmem_ld_n<KH>(cb, part);
       tmem_ld_wait();
 #pragma unroll
-      for (int j0 = 0; j0 < KH; j0 += 4) {
-        float y[4];
-        tmem_ld<4>(cb + KP + j0, y);
+      for (int j0 = 0; j0 < KH; j0 += 8) {  // the W_lo columns, 8 at a time (register budget)
+        float y[8];
+        if (j0 + 8 <= KH) tmem_ld<8>(cb + KP + j0, y);
+        else tmem_ld<4>(cb + KP + j0, y);
         tmem_ld_wait();
 #pragma unroll
-        for (int j = 0; j < 4; ++j) part[j0 + j] += y[j];
+        for (int j = 0; j < 8; ++j)
+          if (j0 + j < KH) part[j0 + j] += y[j];
       }
       tc_fence_before();
-      // lane m = 32q + lane of D_B: m < 64 -> num of frame m, else den of frame m - 64
-      const int m = 32 * q + lane, nd = m >> 6, n = m & 63;
       float* dst = XB + ((int(rank) * 2 + nd) * kPcFrames + n) * XS + KH * hh;
 #pragma unroll
       for (int j = 0; j < KH; j += 4)
@@ -796,8 +802,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPcThreads, 1) solve
     }
     proxy_fence();  // the partials, for the bulk copy (async proxy)
     __syncthreads();
+    PC_MARK(16, 0);
     if (tid == 0) {  // our partials -> the same place in the peer's slots (num rows, den rows)
-      mbar_wait_cluster(&bar_pfree, pass & 1);
+      const uint32_t xrow_bytes = uint32_t(nf * XS * sizeof(float));
+      mbar_wait_cluster(&bar_pfree, pass & 1);  // the peer's phase B is done: its slots are free
       PC_MARK(9, 0);
       const uint32_t rbar = dsmem_addr(&bar_xfull, peer);
 #pragma unroll
@@ -810,37 +818,60 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPcThreads, 1) solve
             : "memory");
       }
     }
-    PC_MARK(16, 0);
-    mbar_wait_cluster(&bar_xfull, pass & 1);
+    mbar_wait_cluster(&bar_xfull, pass & 1);  // the peer's partials have landed
     PC_MARK(12, 0);
-    // both CTAs: h of every frame, fixed order (own-rank-independent: rank 0 + rank 1 + tail)
-    const int nk4 = (K + 3) >> 2;  // frames >= nf and atoms >= K keep h = 0
-    for (int it = tid; it < nf * nk4; it += kPcThreads) {
-      // frame-fastest: a quarter warp touches 8 consecutive frames, conflict-free in both
-      // the exchange rows (stride XS) and the h core matrices
-      const int k4 = 4 * (it / nf), n = it - (it / nf) * nf;
-      const float4 a0 = *reinterpret_cast<const float4*>(XB + (0 * kPcFrames + n) * XS + k4);
-      const float4 a1 = *reinterpret_cast<const float4*>(XB + (2 * kPcFrames + n) * XS + k4);
-      const float4 b0 = *reinterpret_cast<const float4*>(XB + (1 * kPcFrames + n) * XS + k4);
-      const float4 b1 = *reinterpret_cast<const float4*>(XB + (3 * kPcFrames + n) * XS + k4);
-      float num[4] = {a0.x + a1.x, a0.y + a1.y, a0.z + a1.z, a0.w + a1.w};
-      float den[4] = {b0.x + b1.x, b0.y + b1.y, b0.z + b1.z, b0.w + b1.w};
-      for (int i = 0; i < ntail; ++i) {
-        const float qt = Qt[i * kPcFrames + n], rt = Rt[i * kPcFrames + n];
+    {
+      // both CTAs: h of every frame, fixed order (own-rank-independent: rank 0 + rank 1 + tail);
+      // thread (frame n = tid % 64, k quads g, g + 4, ...) loads all its operands first.  A
+      // quarter warp touches 8 consecutive frames: conflict-free in the exchange rows (stride
+      // XS) and in the h core matrices.  Frames >= nf and atoms >= K keep h = 0.
+      constexpr int NQ = KP / 4, NI = (NQ + 3) / 4;
+      const int n = tid & 63, g = tid >> 6, nk4 = (K + 3) >> 2;
+      // two quads at a time (register budget: v + eps stays resident)
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          num[e] = fmaf(Wt[i * KP + k4 + e], qt, num[e]);
-          den[e] = fmaf(Wt[i * KP + k4 + e], rt, den[e]);
+      for (int i0 = 0; i0 < NI; i0 += 2) {
+        if (n >= nf) break;
+        float4 a0[2], a1[2], b0[2], b1[2], hq[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int kq = g + 4 * (i0 + i), k4 = 4 * kq;
+          if (i0 + i < NI && kq < nk4) {
+            a0[i] = *reinterpret_cast<const float4*>(XB + (0 * kPcFrames + n) * XS + k4);
+            a1[i] = *reinterpret_cast<const float4*>(XB + (2 * kPcFrames + n) * XS + k4);
+            b0[i] = *reinterpret_cast<const float4*>(XB + (1 * kPcFrames + n) * XS + k4);
+            b1[i] = *reinterpret_cast<const float4*>(XB + (3 * kPcFrames + n) * XS + k4);
+            hq[i] = *reinterpret_cast<const float4*>(Hh + pc_off_h<KP>(n, k4));
+          }
+        }
+        PC_MARK(34, i0);
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int kq = g + 4 * (i0 + i), k4 = 4 * kq;
+          if (i0 + i >= NI || kq >= nk4) continue;
+          float num[4] = {a0[i].x + a1[i].x, a0[i].y + a1[i].y, a0[i].z + a1[i].z, a0[i].w + a1[i].w};
+          float den[4] = {b0[i].x + b1[i].x, b0[i].y + b1[i].y, b0[i].z + b1[i].z, b0[i].w + b1[i].w};
+#pragma unroll
+          for (int r = 0; r < kPcMaxTail; ++r) {  // (unrolled: no runtime-trip loop in the update)
+            if (r >= ntail) break;
+            const float qt = Qt[r * kPcFrames + n], rt = Rt[r * kPcFrames + n];
+            const float4 wt = *reinterpret_cast<const float4*>(Wt + r * KP + k4);
+            const float w4[4] = {wt.x, wt.y, wt.z, wt.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              num[e] = fmaf(w4[e], qt, num[e]);
+              den[e] = fmaf(w4[e], rt, den[e]);
+            }
+          }
+          float hv[4] = {hq[i].x, hq[i].y, hq[i].z, hq[i].w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (k4 + e < K) hv[e] = hv[e] * sqrt_approx(num[e] * rcp_approx(den[e]));
+          const int o = pc_off_h<KP>(n, k4);
+          *reinterpret_cast<float4*>(Hh + o) = make_float4(hv[0], hv[1], hv[2], hv[3]);
+          *reinterpret_cast<float4*>(Hl + o) =
+              make_float4(tf32_lo(hv[0]), tf32_lo(hv[1]), tf32_lo(hv[2]), tf32_lo(hv[3]));
         }
       }
-      const int o = pc_off_h<KP>(n, k4);
-      float4 h = *reinterpret_cast<const float4*>(Hh + o);
-      float hv[4] = {h.x, h.y, h.z, h.w};
-#pragma unroll
-      for (int e = 0; e < 4; ++e)
-        if (n < nf && k4 + e < K) hv[e] = hv[e] * sqrt_approx(num[e] * rcp_approx(den[e]));
-      *reinterpret_cast<float4*>(Hh + o) = make_float4(hv[0], hv[1], hv[2], hv[3]);
-      *reinterpret_cast<float4*>(Hl + o) = make_float4(tf32_lo(hv[0]), tf32_lo(hv[1]), tf32_lo(hv[2]), tf32_lo(hv[3]));
     }
     PC_MARK(17, 0);
     proxy_fence();

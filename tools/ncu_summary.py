@@ -28,7 +28,8 @@ want = ["gpu__time_duration.sum", "sm__throughput.avg.pct_of_peak_sustained_elap
         "sm__ops_path_tensor_src_tf32_dst_fp32.avg.pct_of_peak_sustained_elapsed",
         "sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active",
         "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
-        "sm__inst_executed_pipe_tc.avg.pct_of_peak_sustained_active"]
+        "sm__inst_executed_pipe_tc.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active", "sm__pipe_xu_cycles_active.avg.pct_of_peak_sustained_active"]
 for w in want:
     if w in h:
         print(f"{w:70s} {v[h.index(w)]} {u[h.index(w)]}")
