@@ -262,7 +262,7 @@ static_assert(MmShape<7, 2, 12>::HF == 2 * 7 * 256, "K1M fragment copy = mma_sme
 bool mma_configured[2][2][7] = {};
 // ISNMF_MMA=0 keeps K <= 56 on the FFMA register-tile kernels; otherwise K1M is
 // used when a CTA gets at least ISNMF_MMA_MIN frames (default 1)
-int mma_warps() {  // ISNMF_MMA_WARPS = 8 or 12 (default 12 when the CTA fits)
+int mma_warps() {  // ISNMF_MMA_WARPS = 8 or 12 (default 12 when the CTA fits; 16 measured slower at config 1)
   static const int v = [] {
     const char* e = getenv("ISNMF_MMA_WARPS");
     return (e && atoi(e) == 8) ? 8 : 12;
@@ -336,7 +336,15 @@ int plan_solve(int64_t F, int64_t K, int64_t frames, SolvePlan* plan, bool force
   }
   if (!force_generic && K >= 1 && K <= 56) {
     const int64_t per_cta = (frames + device_sms() - 1) / device_sms();
-    const int nt = int(std::min<int64_t>(32, std::max<int64_t>(1, per_cta)));
+    // one frame group (<= 16 frames per CTA): fill it.  A K1M pass over one frame group costs
+    // the same at 1 and 16 frames (the MMA tile is 16 frames either way), and fewer CTAs mean
+    // fewer statistics planes for K2 to fold (config 1: 143 -> 63 planes, 17.8 -> 15.9 us).
+    // ISNMF_MMA_NT overrides the floor (A/B measurement only).
+    static const int nt_min = [] {
+      const char* e = getenv("ISNMF_MMA_NT");
+      return e ? atoi(e) : 16;
+    }();
+    const int nt = int(std::min<int64_t>(32, std::max<int64_t>(std::max(1, per_cta <= 16 ? nt_min : 1), per_cta)));
     const int kb = int((K + 7) / 8), fg = nt > 16 ? 2 : 1;
     int nw = mma_warps();
     if (nw == 12 && mma_smem(kb, fg, 12, int(F)) + 2048 > size_t(smem_optin())) nw = 8;

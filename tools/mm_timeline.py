@@ -15,7 +15,7 @@ from tools.synth import spectrogram_torch, w_init  # noqa: E402
 
 L = E.lib()
 L.isnmf_debug_phase_prof.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32]
-F, K, beta, iters = 513, 50, 4096, 10
+F, K, beta, iters = (int(x) for x in sys.argv[1:5]) if len(sys.argv) > 4 else (513, 50, 4096, 10)
 N = beta * 3
 vd = spectrogram_torch(F, K, N, seed=1)
 torch.cuda.synchronize()
