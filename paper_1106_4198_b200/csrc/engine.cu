@@ -152,6 +152,27 @@ cudaError_t launch_pdl(void (*fn)(P...), int grid, int block, size_t smem, cudaS
   return cudaLaunchKernelEx(&cfg, fn, std::forward<A>(args)...);
 }
 
+// launch on 2-CTA clusters (K1P), with programmatic dependent launch when pdl
+template <class... P, class... A>
+cudaError_t launch_cluster2(void (*fn)(P...), int grid, int block, size_t smem, cudaStream_t s, bool pdl,
+                            A&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(grid));
+  cfg.blockDim = dim3(unsigned(block));
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 2 : 1;
+  return cudaLaunchKernelEx(&cfg, fn, std::forward<A>(args)...);
+}
+
 // Growth factor of the host-frame chunk ramp.  A chunk of r*s frames must copy in
 // about the compute time of the previous s frames: copy/compute per frame is
 // ~ (4F B / 50 GB/s) / (6FK(I+1) flop / 45 TFLOP/s) = 600 / (K (I+1)), so r =
@@ -252,10 +273,11 @@ bool tc_enabled() {
 }
 
 // K1M: all-tensor-pipe solve for K <= 56 (instantiated in csrc/mma_table.cu)
-size_t mma_smem(int kb, int fg, int nw, int F) {
+size_t mma_smem(int kb, int fg, int nw, int F, bool pair2 = false) {
   const int KP = 8 * kb, NT = 16 * fg, WS = mm_stride(KP), HT = mm_stride(NT);
   const size_t F16 = size_t((F + 15) & ~15), red = size_t(nw) * 8 * kb * 32, ht = size_t(KP) * HT;
-  return sizeof(float) * (F16 * WS + size_t(fg) * kb * 256 + (red > ht ? red : ht));
+  const size_t xr = pair2 ? size_t(2 * 2 * 32 * kb * 8) : 0;  // K1P exchange (MmShape::XR_FLOATS)
+  return sizeof(float) * (F16 * WS + size_t(fg) * kb * 256 + (red > ht ? red : ht) + xr);
 }
 static_assert(MmShape<7, 2, 12>::WS == 56 && MmShape<7, 2, 12>::HT == 40, "K1M strides");
 static_assert(MmShape<7, 2, 12>::HF == 2 * 7 * 256, "K1M fragment copy = mma_smem()");
@@ -282,6 +304,7 @@ int mma_min_frames() {
 struct SolvePlan {
   bool tiled = false;       // the kernel loops over frame tiles (K1M): any grid <= tiles works
   bool pair = false;        // K1C: one 2-CTA cluster per NT frames (grid = 2 x blocks, two divergence partials each)
+  bool mpair = false;       // K1P: K1M on 2-CTA clusters (rows split), same grid / partial counts as K1C
   LargeFn large = nullptr;  // tensor-pipe kernels (large K, or the resident-dictionary variant)
   LargeFn multi = nullptr;  // K1M's multi-tile instantiation (grid < tiles)
   int threads = 0;          // block size of `large`
@@ -304,6 +327,16 @@ int pair_mode(int flags = 0) {
   return v;
 }
 bool pair_configured[8] = {};
+// K1P (K1M rows split over a 2-CTA cluster): ISNMF_K1P = 0 off, 1 (default) for online
+// mini-batches whose K1M CTAs would hold one frame group (<= 16 frames per CTA)
+int mpair_mode(int flags = 0) {
+  static const int v = [] {
+    const char* e = getenv("ISNMF_K1P");
+    return e ? atoi(e) : 1;
+  }();
+  if (flags & ISNMF_FLAG_NO_PAIR) return 0;
+  return v;
+}
 
 int plan_solve(int64_t F, int64_t K, int64_t frames, SolvePlan* plan, bool force_generic = false,
                bool allow_pair = false, int flags = 0) {
@@ -347,8 +380,12 @@ int plan_solve(int64_t F, int64_t K, int64_t frames, SolvePlan* plan, bool force
     const int nt = int(std::min<int64_t>(32, std::max<int64_t>(std::max(1, per_cta <= 16 ? nt_min : 1), per_cta)));
     const int kb = int((K + 7) / 8), fg = nt > 16 ? 2 : 1;
     int nw = mma_warps();
-    if (nw == 12 && mma_smem(kb, fg, 12, int(F)) + 2048 > size_t(smem_optin())) nw = 8;
-    const size_t smem = mma_smem(kb, fg, nw, int(F));
+    // K1P: one frame group per pair of SMs (online, enough SMs for every pair)
+    const int pairs = int((frames + nt - 1) / nt);
+    const bool mp = allow_pair && !force_generic && fg == 1 && nw == 12 && mpair_mode(flags) != 0 &&
+                    2 * pairs <= device_sms();
+    if (nw == 12 && mma_smem(kb, fg, 12, int(F), mp) + 2048 > size_t(smem_optin())) nw = 8;
+    const size_t smem = mma_smem(kb, fg, nw, int(F), mp && nw == 12);
     const int wi = nw == 12 ? 1 : 0;
     if (nt >= mma_min_frames() && smem + 2048 <= size_t(smem_optin())) {
       if (!mma_configured[wi][fg - 1][kb - 1]) {
@@ -360,6 +397,7 @@ int plan_solve(int64_t F, int64_t K, int64_t frames, SolvePlan* plan, bool force
       plan->large = mma_kernel(nw, fg, kb, false);
       plan->multi = mma_kernel(nw, fg, kb, true);
       plan->tiled = true;
+      plan->mpair = mp && nw == 12;
       plan->threads = 32 * nw;
       plan->var = nullptr;
       plan->NT = nt;
@@ -442,8 +480,11 @@ void launch_solve(const SolvePlan& p, int nblk, const SolveArgs& args, cudaStrea
   SolveArgs a = args;
   a.cta_frames = p.NT;
   const LargeFn large = (p.multi && int64_t(nblk) * p.NT < a.nframes) ? p.multi : p.large;
-  if (p.pair) nblk *= 2;  // one 2-CTA cluster per block of NT frames
-  if (large && pdl && pdl_enabled())
+  if (p.pair || p.mpair) nblk *= 2;  // one 2-CTA cluster per block of NT frames
+  a.pair2 = p.mpair ? 1 : 0;
+  if (p.mpair)
+    launch_cluster2(p.large, nblk, p.threads, p.smem, s, pdl && pdl_enabled(), a);
+  else if (large && pdl && pdl_enabled())
     launch_pdl(large, nblk, p.threads, p.smem, s, a);
   else if (large)
     large<<<nblk, p.threads, p.smem, s>>>(a);
@@ -733,7 +774,7 @@ int launch_block(isnmf_online* c, const float* dv, int64_t ldv, int nb, const ui
   const bool commit = (c->t_host + uint64_t(nb)) % uint64_t(c->beta) == 0;
   FoldArgs r = fold_args(c);
   r.nstat = nblk;
-  r.ndiv = c->plan.pair ? 2 * nblk : nblk;
+  r.ndiv = (c->plan.pair || c->plan.mpair) ? 2 * nblk : nblk;
   r.nframes = nb;
   r.do_commit = commit;
   r.eta = c->eta;
@@ -1238,6 +1279,7 @@ int isnmf_online_solver(isnmf_online* c, char* buf, int64_t cap) {
   if (!c || !buf || cap < 1) return fail(ISNMF_E_INVALID_ARG, "online_solver: NULL argument");
   const SolvePlan& p = c->plan;
   const char* name = p.pair                                      ? "K1C"
+                     : p.mpair                                   ? "K1P"
                      : p.tiled                                   ? "K1M"
                      : p.var                                     ? "K1"
                      : p.large && p.threads == kTcThreads        ? "K1T"

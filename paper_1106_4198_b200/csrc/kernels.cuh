@@ -153,6 +153,7 @@ struct SolveArgs {
   int64_t v0;           // frame(n) = v0 + n when vsel == nullptr
   int nframes;
   int cta_frames;  // frames per CTA of runtime-shaped kernels (K1M); set by launch_solve
+  int pair2;       // K1M, one frame group: the frames' rows split over a 2-CTA cluster (K1P)
   int iters;
   float eps;
   double epsd;

@@ -60,11 +60,12 @@ struct MmShape {
   static constexpr int HT = mm_stride(NT);
   static constexpr int NREG = 8 * KB;         // num + den accumulator floats per lane
   static constexpr int HF = FG * KB * 32 * 8;  // h^T A fragments, [fm][kb][lane][hi 4 | lo 4]
-  static size_t smem_bytes(int F) {
+  // num/den partials [NW][NREG][32] | h^T [KP][HT] (statistics pass)
+  static constexpr int RED_FLOATS = NW * NREG * 32 > KP * HT ? NW * NREG * 32 : KP * HT;
+  static constexpr int XR_FLOATS = 2 * 2 * 32 * KB * 8;  // K1P exchange [parity][rank][record][num 4 | den 4]
+  static size_t smem_bytes(int F, bool pair2 = false) {
     const size_t F16 = size_t((F + 15) & ~15);
-    const size_t red = size_t(NW) * NREG * 32;
-    const size_t ht = size_t(KP) * HT;
-    return sizeof(float) * (F16 * WS + HF + (red > ht ? red : ht));
+    return sizeof(float) * (F16 * WS + HF + RED_FLOATS + (pair2 ? XR_FLOATS : 0));
   }
 };
 
@@ -429,9 +430,34 @@ __global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a
   constexpr int KP = S::KP, NT = S::NT, RG = S::RG, WS = S::WS, HT = S::HT, NREG = S::NREG;
   constexpr int kMmThreads = 32 * NW;
   MM_STAMP(62);
+  if constexpr (!MULTI && FG == 1)
+    if (a.pair2) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");  // (waited below)
   pdl_wait();
   MM_STAMP(58);
-  if (*a.status || (a.halt && *a.halt)) return;
+  // K1P (a.pair2; online, one frame group): a 2-CTA cluster shares the tile's frames, rank r
+  // owning the rows of 16-row blocks [r * S16, ...) — the num/den partials of the two row halves
+  // are exchanged through distributed shared memory once per pass, so both CTAs apply the same
+  // fixed-order update (rank 0 + rank 1) and hold the same h
+  constexpr bool kCanPair = !MULTI && FG == 1;
+  const bool pair2 = kCanPair && a.pair2 != 0;
+  const unsigned crank = pair2 ? cluster_rank() : 0u;
+  if constexpr (kCanPair) {
+    if (pair2) {  // both CTAs take the same go decision (a status bit set meanwhile must not split them)
+      __shared__ int s_go2[2];
+      asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // the peer has started
+      if (threadIdx.x == 0) {
+        const int go = !(*a.status || (a.halt && *a.halt));
+        s_go2[crank] = go;
+        *const_cast<int*>(map_rank(&s_go2[crank], crank ^ 1u)) = go;
+      }
+      cluster_sync_all();
+      if (!(s_go2[0] && s_go2[1])) return;
+    } else if (*a.status || (a.halt && *a.halt)) {
+      return;
+    }
+  } else {
+    if (*a.status || (a.halt && *a.halt)) return;
+  }
 
   extern __shared__ __align__(16) float smem[];
   const int F = a.F, K = a.K;
@@ -454,7 +480,8 @@ __global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a
   // frame tiles of ntc frames; CTA b owns tiles b, b + gridDim.x, ... (one tile per CTA
   // for an online mini-batch; the batch path runs one CTA per SM over all N frames, so
   // the dictionary is loaded once per CTA and the statistics planes accumulate in place)
-  const int ntiles = MULTI ? (a.nframes + ntc - 1) / ntc : int(blockIdx.x) + 1;
+  const int tile0 = pair2 ? int(blockIdx.x >> 1) : int(blockIdx.x);
+  const int ntiles = MULTI ? (a.nframes + ntc - 1) / ntc : tile0 + 1;
 
   if (tid == 0) {  // dictionary -> smem by TMA bulk copies, overlapped with the h0 set-up below
     const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&wbar));
@@ -480,7 +507,7 @@ __global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a
   // (every tile but the last stages its successor, so tile i > 0 finds its H0 staged)
   const bool stage_next = MULTI && a.h0_mode == 0 && !a.vsel && int(gridDim.x) < ntiles;
   float* Hstage = RED + ((KP * HT + 31) & ~31);
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  for (int tile = tile0; tile < ntiles; tile += gridDim.x) {
   const bool first_tile = !MULTI || tile == int(blockIdx.x);
   const bool staged = stage_next && !first_tile;
   const int n0 = tile * ntc;
@@ -550,7 +577,11 @@ __global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a
   const int fm = warp / RG, rq = warp % RG;
   const int rgi = (FG == 2 && fm == 1) ? RG - 1 - rq : rq;
   const int NBLK = (F + 7) >> 3;
-  const int blk0 = rgi * NBLK / RG, blk1 = (rgi + 1) * NBLK / RG;
+  // rows of this CTA: all, or (K1P) 16-row blocks [M0, M1) = 8-row blocks [B0, B1)
+  const int NB16 = F16 / 16, S16 = (NB16 + 1) / 2;
+  const int M0 = pair2 ? int(crank) * S16 : 0, M1 = pair2 ? (crank ? NB16 : S16) : NB16;
+  const int B0 = 2 * M0, B1 = pair2 ? min(NBLK, 2 * M1) : NBLK, NBL = B1 - B0;
+  const int blk0 = B0 + rgi * NBL / RG, blk1 = B0 + (rgi + 1) * NBL / RG;
   const int nA = 16 * fm + g, nB = nA + 8;
   const bool okA = nA < nf, okB = nB < nf;
   const float* pA = fptr[nA];
@@ -600,43 +631,86 @@ __global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a
     // thread per (k block, lane) record = 4 cells, h read from / written to the fragment copy
     constexpr int RECS = 32 * KB;  // per frame group, over its RG * 32 threads
     const int gt = tid - fm * RG * 32;
+    auto rec_sum = [&](int p, float4& num, float4& den) {
+      const int ln = p & 31, jb = p >> 5;
+      num = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+      den = num;
 #pragma unroll
-    for (int m = 0; m < (RECS + RG * 32 - 1) / (RG * 32); ++m) {
-      const int p = gt + m * RG * 32;
-      if (p < RECS) {
-        const int ln = p & 31, jb = p >> 5;
-        float4 num = make_float4(0.0f, 0.0f, 0.0f, 0.0f), den = num;
+      for (int r = 0; r < RG; ++r) {
+        const float* src = RED + (fm * RG + r) * NREG * 32 + jb * 128 + ln * 4;
+        const float4 x = *reinterpret_cast<const float4*>(src);
+        const float4 y = *reinterpret_cast<const float4*>(src + KB * 128);
+        num.x += x.x;
+        num.y += x.y;
+        num.z += x.z;
+        num.w += x.w;
+        den.x += y.x;
+        den.y += y.y;
+        den.z += y.z;
+        den.w += y.w;
+      }
+    };
+    auto rec_update = [&](int p, const float4& num, const float4& den) {
+      const int ln = p & 31, jb = p >> 5;
+      // C order (c0 (g, 2t), c1 (g, 2t+1), c2 (g+8, 2t), c3 (g+8, 2t+1)) -> record order a0 a2 a1 a3
+      float* rec = Hf + (fm * KB + jb) * 256 + ln * 4;
+      float4 h = *reinterpret_cast<const float4*>(rec);
+      const int n0c = 16 * fm + (ln >> 2), k0c = 8 * jb + 2 * (ln & 3);
+      const bool v0 = n0c < nf, v1 = n0c + 8 < nf, e0 = k0c < K, e1 = k0c + 1 < K;
+      h.x = (v0 && e0) ? h.x * sqrt_approx(num.x * rcp_approx(den.x)) : h.x;
+      h.z = (v0 && e1) ? h.z * sqrt_approx(num.y * rcp_approx(den.y)) : h.z;
+      h.y = (v1 && e0) ? h.y * sqrt_approx(num.z * rcp_approx(den.z)) : h.y;
+      h.w = (v1 && e1) ? h.w * sqrt_approx(num.w * rcp_approx(den.w)) : h.w;
+      uint32_t hi, lo[4];
+      split_tf32(h.x, hi, lo[0]);
+      split_tf32(h.y, hi, lo[1]);
+      split_tf32(h.z, hi, lo[2]);
+      split_tf32(h.w, hi, lo[3]);
+      *reinterpret_cast<float4*>(rec) = h;
+      *reinterpret_cast<float4*>(rec + 128) = make_float4(__uint_as_float(lo[0]), __uint_as_float(lo[1]),
+                                                          __uint_as_float(lo[2]), __uint_as_float(lo[3]));
+    };
+    // fixed-order sum over the RG row groups, h *= sqrt(num/den) (kernels.hpp:77); one
+    // thread per (k block, lane) record = 4 cells, h read from / written to the fragment copy
+    if (!pair2) {
 #pragma unroll
-        for (int r = 0; r < RG; ++r) {
-          const float* src = RED + (fm * RG + r) * NREG * 32 + jb * 128 + ln * 4;
-          const float4 x = *reinterpret_cast<const float4*>(src);
-          const float4 y = *reinterpret_cast<const float4*>(src + KB * 128);
-          num.x += x.x;
-          num.y += x.y;
-          num.z += x.z;
-          num.w += x.w;
-          den.x += y.x;
-          den.y += y.y;
-          den.z += y.z;
-          den.w += y.w;
+      for (int m = 0; m < (RECS + RG * 32 - 1) / (RG * 32); ++m) {
+        const int p = gt + m * RG * 32;
+        if (p < RECS) {
+          float4 num, den;
+          rec_sum(p, num, den);
+          rec_update(p, num, den);
         }
-        // C order (c0 (g, 2t), c1 (g, 2t+1), c2 (g+8, 2t), c3 (g+8, 2t+1)) -> record order a0 a2 a1 a3
-        float* rec = Hf + (fm * KB + jb) * 256 + ln * 4;
-        float4 h = *reinterpret_cast<const float4*>(rec);
-        const int n0c = 16 * fm + (ln >> 2), k0c = 8 * jb + 2 * (ln & 3);
-        const bool v0 = n0c < nf, v1 = n0c + 8 < nf, e0 = k0c < K, e1 = k0c + 1 < K;
-        h.x = (v0 && e0) ? h.x * sqrt_approx(num.x * rcp_approx(den.x)) : h.x;
-        h.z = (v0 && e1) ? h.z * sqrt_approx(num.y * rcp_approx(den.y)) : h.z;
-        h.y = (v1 && e0) ? h.y * sqrt_approx(num.z * rcp_approx(den.z)) : h.y;
-        h.w = (v1 && e1) ? h.w * sqrt_approx(num.w * rcp_approx(den.w)) : h.w;
-        uint32_t hi, lo[4];
-        split_tf32(h.x, hi, lo[0]);
-        split_tf32(h.y, hi, lo[1]);
-        split_tf32(h.z, hi, lo[2]);
-        split_tf32(h.w, hi, lo[3]);
-        *reinterpret_cast<float4*>(rec) = h;
-        *reinterpret_cast<float4*>(rec + 128) = make_float4(__uint_as_float(lo[0]), __uint_as_float(lo[1]),
-                                                            __uint_as_float(lo[2]), __uint_as_float(lo[3]));
+      }
+    } else if constexpr (kCanPair) {
+      // K1P: this CTA's row-half sums -> XR[pass & 1][rank] here and in the peer (DSMEM),
+      // cluster barrier, then rank 0 + rank 1 in that order in both CTAs.  Double-buffered by
+      // pass parity: the peer writes a buffer again two passes later, past the next barrier.
+      float4* XR = reinterpret_cast<float4*>(RED + S::RED_FLOATS) + (pass & 1) * 2 * 2 * RECS;
+#pragma unroll
+      for (int m = 0; m < (RECS + RG * 32 - 1) / (RG * 32); ++m) {
+        const int p = gt + m * RG * 32;
+        if (p < RECS) {
+          float4 num, den;
+          rec_sum(p, num, den);
+          float4* own = XR + (crank * RECS + p) * 2;
+          own[0] = num;
+          own[1] = den;
+          float4* far = const_cast<float4*>(map_rank(own, crank ^ 1u));
+          far[0] = num;
+          far[1] = den;
+        }
+      }
+      cluster_sync_all();
+#pragma unroll
+      for (int m = 0; m < (RECS + RG * 32 - 1) / (RG * 32); ++m) {
+        const int p = gt + m * RG * 32;
+        if (p < RECS) {
+          const float4 n0v = XR[p * 2], d0v = XR[p * 2 + 1];
+          const float4 n1v = XR[(RECS + p) * 2], d1v = XR[(RECS + p) * 2 + 1];
+          rec_update(p, make_float4(n0v.x + n1v.x, n0v.y + n1v.y, n0v.z + n1v.z, n0v.w + n1v.w),
+                     make_float4(d0v.x + d1v.x, d0v.y + d1v.y, d0v.z + d1v.z, d0v.w + d1v.w));
+        }
       }
     }
     MM_STAMP(3 + 4 * pass);
@@ -667,21 +741,27 @@ __global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a
     __syncthreads();
     const int FP = (F + 3) & ~3;
     ISNMF_DASSERT(!a.stats || a.stats_cap == 0 || int(blockIdx.x) < a.stats_cap);
-    float* outA = a.stats ? a.stats + size_t(blockIdx.x) * 2 * FP * KP : nullptr;
+    // (K1P: the pair's plane, this CTA's rows)
+    float* outA = a.stats ? a.stats + size_t(pair2 ? tile : int(blockIdx.x)) * 2 * FP * KP : nullptr;
     float* outB = a.stats ? outA + size_t(FP) * KP : nullptr;
     float vv[2 * FG][4];
-    if (warp < F16 / 16) mm_stats_v<2 * FG>(vv, fptr, 16 * warp, F, nf, g, t);
+    if (M0 + warp < M1) mm_stats_v<2 * FG>(vv, fptr, 16 * (M0 + warp), F, nf, g, t);
 #pragma unroll 1
-    for (int m = warp; m < F16 / 16; m += kMmThreads / 32) {
+    for (int m = M0 + warp; m < M1; m += kMmThreads / 32) {
       const int mn = m + kMmThreads / 32;
       mm_stats_block<KB, FG, WS, HT>(Ws, Hf, Ht, fptr, 16 * m, F, nf, eps, g, t, want_div, divacc, outA, outB,
-                                         FP, vv, mn < F16 / 16 ? 16 * mn : -1, a.prof,
-                                         44 + 4 * ((m - warp) / (kMmThreads / 32)), !first_tile);
+                                         FP, vv, mn < M1 ? 16 * mn : -1, a.prof,
+                                         44 + 4 * ((m - M0 - warp) / (kMmThreads / 32)), !first_tile);
     }
   }
   divd += double(divacc);
 
-  write_final_h(a, n0, nf, [&](int n, int k) { return Hf[hf_index<KB>(n, k)]; });
+  if (!pair2) {
+    write_final_h(a, n0, nf, [&](int n, int k) { return Hf[hf_index<KB>(n, k)]; });
+  } else {  // K1P: both CTAs hold every frame's h; each writes half of the frames
+    const int half = (nf + 1) / 2, f0 = crank ? half : 0, fc = crank ? nf - half : half;
+    write_final_h(a, n0 + f0, fc, [&](int n, int k) { return Hf[hf_index<KB>(f0 + n, k)]; });
+  }
   }  // tiles
 
   MM_STAMP(61);
@@ -694,9 +774,11 @@ __global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a
     if (tid == 0) {
       double s = 0.0;
       for (int w = 0; w < kMmThreads / 32; ++w) s += red[w];
-      a.divpart[blockIdx.x] = s;
+      a.divpart[blockIdx.x] = s;  // (K1P: two partials per pair, 2 * pair + rank)
     }
   }
+  if constexpr (kCanPair)
+    if (pair2) cluster_sync_all();  // no DSMEM access may reach an exited CTA
 
   MM_STAMP(63);
 }

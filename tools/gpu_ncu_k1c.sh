@@ -1,5 +1,5 @@
 #!/bin/bash
-# ncu --set full (with source) of one K1C launch at config 3
+# ncu --set full (with source) of one K1C launch at config 3, after the same command ran clean
 mkdir -p gpurun_out
 ARGS="--steps 1 --warmup 1 --frames 409600 --no-e2e --no-cpu --no-compare"
 python bench.py $ARGS > gpurun_out/plain_k1c.log 2>&1 && \
