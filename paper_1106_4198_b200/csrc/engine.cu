@@ -561,6 +561,8 @@ int status_to_code(unsigned int s, const char* where, unsigned long long t) {
     return fail(ISNMF_E_NUMERICAL_FAILURE, "%s: non-finite dictionary update at t = %llu", where, t);
   if (s & ST_ZERO_COLUMN) return fail(ISNMF_E_ZERO_COLUMN, "rescale_dictionary: dead atom (t = %llu)", t);
   if (s & ST_DIVERGED) return fail(ISNMF_E_DIVERGED_OBJECTIVE, "%s: objective increased", where);
+  if (s & ST_CHAIN_TIMEOUT)
+    return fail(ISNMF_E_CUDA, "%s: statistics chain timed out (t = %llu)", where, t);
   return fail(ISNMF_E_CUDA, "%s: unknown device status %u", where, s);
 }
 

@@ -39,6 +39,7 @@ enum : uint32_t {
   ST_NONFINITE_W = 4u,
   ST_ZERO_COLUMN = 8u,
   ST_DIVERGED = 16u,
+  ST_CHAIN_TIMEOUT = 32u,  // a statistics-chain predecessor never published its window (K1T)
 };
 
 // Device-resident scalar state of an online / batch context.
@@ -177,6 +178,12 @@ struct SolveArgs {
   float* stats;     // [gridDim][2][KP][FP], FP = F rounded up to 4
   double* divpart;  // [gridDim]
   int stats_cap;    // planes / divergence partials allocated (debug checks; 0 = unchecked)
+  // K1T statistics chain: CTAs b with the same b / chain share plane b / chain; rank b % chain
+  // adds its window tile (rank 0 stores, the others red.add) once rank - 1 has published that
+  // window through chain_flags[b - 1][warp] >= chain_base + window + 1 (fixed order per cell)
+  int chain;                   // CTAs per plane (<= 1: one plane per CTA)
+  uint32_t chain_base;         // 64 x the launch's chain epoch
+  uint32_t* chain_flags;       // [gridDim][8 warps]
   unsigned int* status;
   const unsigned int* halt;
   long long* prof;  // phase cycle counters (ISNMF_PHASE_PROF builds only)

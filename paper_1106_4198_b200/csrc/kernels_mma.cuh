@@ -740,8 +740,8 @@ __global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a
     }
     __syncthreads();
     const int FP = (F + 3) & ~3;
-    ISNMF_DASSERT(!a.stats || a.stats_cap == 0 || int(blockIdx.x) < a.stats_cap);
     // (K1P: the pair's plane, this CTA's rows)
+    ISNMF_DASSERT(!a.stats || a.stats_cap == 0 || (pair2 ? tile : int(blockIdx.x)) < a.stats_cap);
     float* outA = a.stats ? a.stats + size_t(pair2 ? tile : int(blockIdx.x)) * 2 * FP * KP : nullptr;
     float* outB = a.stats ? outA + size_t(FP) * KP : nullptr;
     float vv[2 * FG][4];
@@ -767,7 +767,7 @@ __global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a
   MM_STAMP(61);
   // divergence partial of this CTA (fixed-order reduction)
   if (a.divpart) {
-    ISNMF_DASSERT(a.stats_cap == 0 || int(blockIdx.x) < a.stats_cap);
+    ISNMF_DASSERT(a.stats_cap == 0 || int(blockIdx.x) < (pair2 ? 2 : 1) * a.stats_cap);  // divpart: 2 x planes
     const double d = warp_sum_d(divd);
     if (lane == 0) red[warp] = d;
     __syncthreads();
