@@ -311,9 +311,19 @@ struct SolvePlan {
   Variant* var = nullptr;  // nullptr: generic
   int NT = 0, KP = 0, WS = 0;
   size_t smem = 0;
+  int chain = 0;            // K1T: CTAs per statistics plane (kernels_large_tc.cuh, statistics chain)
 };
 
 bool generic_configured = false;
+
+// K1T statistics chain: ISNMF_CHAIN = CTAs per plane (default 8; 0 or 1: one plane per CTA)
+int chain_len() {
+  static const int v = [] {
+    const char* e = getenv("ISNMF_CHAIN");
+    return e ? atoi(e) : 8;
+  }();
+  return v;
+}
 
 // K1C (csrc/kernels_tc.cuh): ISNMF_K1C = 0 off, 1 (default) for mini-batches that give a
 // pair of SMs >= 40 frames, 2 at any size (tests)
@@ -431,6 +441,7 @@ int plan_solve(int64_t F, int64_t K, int64_t frames, SolvePlan* plan, bool force
         }
         plan->large = large_tc_kernel(nb);
         plan->threads = kTcThreads;
+        plan->chain = (F + kTcRows - 1) / kTcRows + 2 < int64_t(kTcChainSpan) ? chain_len() : 0;
         plan->var = nullptr;
         plan->NT = 8 * nb;
         plan->KP = 256;
@@ -588,6 +599,8 @@ struct isnmf_online {
   float* stats = nullptr;
   double* divpart = nullptr;
   int maxblk = 0;
+  uint32_t* chain_flags = nullptr;  // K1T statistics chain: one progress word per CTA
+  uint32_t chain_epoch = 0;
   double* U = nullptr;  // warm activation store (fp64, see kernels.cuh warm_value)
   uint32_t* T = nullptr;
   int64_t nstore = 0;
@@ -625,7 +638,7 @@ int online_free(isnmf_online* c) {
   if (c->cs) cudaStreamSynchronize(c->cs);
   if (c->xs) cudaStreamSynchronize(c->xs);
   void* ptrs[] = {c->st, c->W64, c->A, c->B, c->pa, c->pb, c->cta_part, c->P, c->W32, c->WB, c->stats,
-                  c->divpart, c->U, c->T, c->u01, c->Hlast, c->tr_t, c->tr_obj, c->tr_ns, c->vbuf[0],
+                  c->chain_flags, c->divpart, c->U, c->T, c->u01, c->Hlast, c->tr_t, c->tr_obj, c->tr_ns, c->vbuf[0],
                   c->vbuf[1], c->ibuf[0], c->ibuf[1]};
   for (void* p : ptrs) dfree(p);
   for (int i = 0; i < 2; ++i) {
@@ -759,6 +772,16 @@ int launch_block(isnmf_online* c, const float* dv, int64_t ldv, int nb, const ui
   a.status = &c->st->status;
   a.halt = &c->st->halt;
   a.prof = c->phase_prof;
+  const bool chained = c->chain_flags && c->plan.chain > 1 && nblk > 1;
+  if (chained) {  // K1T: `chain` CTAs accumulate one statistics plane in rank order
+    if (c->chain_epoch >= (1u << 18)) {  // keep stale words far behind every future target
+      CU(cudaMemsetAsync(c->chain_flags, 0, size_t(c->maxblk) * sizeof(uint32_t), c->cs));
+      c->chain_epoch = 0;
+    }
+    a.chain = c->plan.chain;
+    a.chain_base = ++c->chain_epoch * kTcChainSpan;
+    a.chain_flags = c->chain_flags;
+  }
   if (c->prof) {
     while (c->ev_pool.size() < c->ev_used + 2) {
       cudaEvent_t e;
@@ -775,7 +798,8 @@ int launch_block(isnmf_online* c, const float* dv, int64_t ldv, int nb, const ui
   }
   const bool commit = (c->t_host + uint64_t(nb)) % uint64_t(c->beta) == 0;
   FoldArgs r = fold_args(c);
-  r.nstat = nblk;
+  r.nstat = chained ? (nblk + c->plan.chain - 1) / c->plan.chain : nblk;
+  r.stats_tiled = chained ? 1 : 0;
   r.ndiv = (c->plan.pair || c->plan.mpair) ? 2 * nblk : nblk;
   r.nframes = nb;
   r.do_commit = commit;
@@ -986,6 +1010,7 @@ int isnmf_online_create(isnmf_online** out, const isnmf_online_config* cfg) {
       (rc = dalloc(&c->W32, size_t(c->F) * c->WS)) ||
       (rc = dalloc(&c->stats, size_t(c->maxblk) * 2 * padded_f(c->F) * c->KP + 4)) ||
       (rc = dalloc(&c->divpart, 2 * size_t(c->maxblk))) ||
+      (c->plan.chain > 1 && (rc = dalloc(&c->chain_flags, size_t(c->maxblk)))) ||
       (c->plan.pair && (rc = dalloc(&c->WB, size_t(2) * 2 * c->KP * kWbRows))) ||
       (rc = dalloc(&c->Hlast, size_t(c->beta) * c->K)))
     return bail(rc);
@@ -1000,6 +1025,7 @@ int isnmf_online_create(isnmf_online** out, const isnmf_online_config* cfg) {
   if (cudaMemcpy(c->st, &h, sizeof(h), cudaMemcpyHostToDevice) != cudaSuccess ||
       cudaMemset(c->W32, 0, size_t(c->F) * c->WS * sizeof(float)) != cudaSuccess ||
       (c->WB && cudaMemset(c->WB, 0, size_t(2) * 2 * c->KP * kWbRows * sizeof(float)) != cudaSuccess) ||
+      (c->chain_flags && cudaMemset(c->chain_flags, 0, size_t(c->maxblk) * sizeof(uint32_t)) != cudaSuccess) ||
       cudaMemset(c->pa, 0, FK * sizeof(double)) != cudaSuccess ||
       cudaMemset(c->pb, 0, FK * sizeof(double)) != cudaSuccess ||
       cudaMemset(c->Hlast, 0, size_t(c->beta) * c->K * sizeof(float)) != cudaSuccess)

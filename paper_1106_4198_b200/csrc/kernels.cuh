@@ -1029,6 +1029,7 @@ struct FoldArgs {
   double* scale_out;  // optional: column scales s_k of this commit (batch H compensation)
   int batch_mode;
   int stats_cap;      // planes / divergence partials allocated (debug checks; 0 = unchecked)
+  int stats_tiled;    // planes in K1T's chained layout: [window of 32 rows][sa|sb][KP][32], rows swizzled by k
   long long p_cap;    // rows of P (debug checks; 0 = unchecked)
   long long* tprof;  // ISNMF_PHASE_PROF builds: [gridDim][8] globaltimer stamps of thread 0
 };
@@ -1142,14 +1143,19 @@ __global__ void __cluster_dims__(kFoldCluster, 1, 1) __launch_bounds__(kFoldThre
   const int FP = (F + 3) & ~3;
   const size_t plane = size_t(FP) * a.KP;
   const int b0 = int((long long)r * a.nstat / kFoldCluster), b1 = int((long long)(r + 1) * a.nstat / kFoldCluster);
+  // plane geometry: [sa|sb][KP][FP], or K1T's chained window tiles (kernels_large_tc.cuh tc_stat_off)
+  const size_t pstride = a.stats_tiled ? size_t((F + 31) / 32) * 2 * a.KP * 32 : 2 * plane;
+  const size_t yoff = a.stats_tiled ? size_t(a.KP) * 32 : plane;
   for (int it = tid; it < NQ * G; it += kFoldThreads) {
     const int q = it % NQ, g = it / NQ;
-    const float* base = a.stats + size_t(k) * FP + 4 * q;
+    const float* base = a.stats_tiled ? a.stats + size_t(q >> 3) * 2 * a.KP * 32 + size_t(k) * 32 +
+                                            ((4 * (q & 7)) ^ (((k >> 1) & 3) << 3))
+                                      : a.stats + size_t(k) * FP + 4 * q;
     double s[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
 #pragma unroll 4
     for (int b = b0 + g; b < b1; b += G) {
-      const float4 x = __ldcg(reinterpret_cast<const float4*>(base + size_t(b) * 2 * plane));
-      const float4 y = __ldcg(reinterpret_cast<const float4*>(base + size_t(b) * 2 * plane + plane));
+      const float4 x = __ldcg(reinterpret_cast<const float4*>(base + size_t(b) * pstride));
+      const float4 y = __ldcg(reinterpret_cast<const float4*>(base + size_t(b) * pstride + yoff));
       s[0] += x.x;
       s[1] += x.y;
       s[2] += x.z;

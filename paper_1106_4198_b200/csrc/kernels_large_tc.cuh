@@ -19,6 +19,8 @@
 //   B = [Q|R], K-major (rows contiguous) in no-swizzle core matrices of 8 n' x 4 rows (128 B).
 #pragma once
 
+#include <type_traits>
+
 #include "kernels_large.cuh"
 
 namespace isnmf_dev {
@@ -80,15 +82,42 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
+// ---- statistics chain (SolveArgs::chain): CTAs b with the same b / chain accumulate one plane.
+// A window's [sa|sb] tile (2 x 256 k x 32 rows, 64 KB) is staged in shared memory (the lo copy of
+// the dictionary window, which the statistics pass does not use: it splits W on the fly) and goes
+// out as TMA bulk copies — rank 0 of a chain stores, the others `cp.reduce.async.bulk ... add.f32`
+// (the addition happens in L2) — once the previous rank has published that window in
+// chain_flags, so every cell is summed in rank order (bitwise reproducible) and a mini-batch
+// leaves gridDim / chain planes for K2 instead of gridDim.
+// Plane layout in chain mode: [window][sa|sb][k][32 rows], rows XOR-swizzled by k (tc_stat_off).
+constexpr int kTcStatTile = 2 * 256 * kTcRows;  // floats of one window tile
+__host__ __device__ __forceinline__ int tc_stat_off(int k, int row) {  // inside one [k][32] half tile
+  return k * kTcRows + (row ^ (((k >> 1) & 3) << 3));
+}
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+constexpr uint32_t kTcChainSpan = 4096;  // flag values per launch epoch: window + 1, span - 1 = abandoned
+constexpr int kTcChainSpins = 1 << 19;  // bounded wait on the previous rank (ST_CHAIN_TIMEOUT)
+
 template <int NB>
 __global__ void __launch_bounds__(kTcThreads, 1) solve_large_tc_kernel(const SolveArgs a) {
   using L = LargeTcShape<NB>;
   constexpr int KP = L::KP, NT = L::NT, N2 = L::N2, KB = L::KB, FMB = L::FMB, TPW = L::TPW, KPS = L::KPS,
                 WS = L::WS, HROWS = L::HROWS, AW = L::AW, BW = L::BW;
   pdl_wait();
-  if (*a.status || (a.halt && *a.halt)) return;
+  const bool chained = a.chain > 1 && a.do_stats && a.stats;
+  if (*a.status || (a.halt && *a.halt)) {
+    // a successor in the statistics chain must never wait for this CTA
+    if (chained && threadIdx.x == 0) st_release_u32(a.chain_flags + blockIdx.x, a.chain_base + kTcChainSpan - 1u);
+    return;
+  }
   extern __shared__ __align__(16) float smem_raw[];
-  // 1024-byte aligned base for the swizzled operand atoms
   // 1024-byte aligned base, as an offset from the shared array (keeps the pointers in the shared space)
   const uint32_t sbase = smem_addr(smem_raw);
   float* smem = smem_raw + ((((sbase + 1023u) & ~1023u) - sbase) >> 2);
@@ -160,6 +189,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) solve_large_tc_kernel(const Sol
                       : make_float4(0.f, 0.f, 0.f, 0.f);
     }
   };
+  // chained statistics pass: the lo copy's space is the staging tile of the window statistics,
+  // and phase A takes the remainders from the hi copy on the fly
+  bool lo_fly = false;
+  auto rem = [](float v) { return v - __uint_as_float(__float_as_uint(v) & 0xffffe000u); };
   auto store_w = [&](int buf) {  // registers -> A hi / lo (MN-major swizzled)
     float* hi = Ahi + buf * AW;
     float* lo = Alo + buf * AW;
@@ -169,8 +202,20 @@ __global__ void __launch_bounds__(kTcThreads, 1) solve_large_tc_kernel(const Sol
       const int o = tc_off_a(k0, row);
       const float4 x = wreg[j];
       *reinterpret_cast<float4*>(hi + o) = x;
-      auto rem = [](float v) { return v - __uint_as_float(__float_as_uint(v) & 0xffffe000u); };
-      *reinterpret_cast<float4*>(lo + o) = make_float4(rem(x.x), rem(x.y), rem(x.z), rem(x.w));
+      if (!lo_fly) *reinterpret_cast<float4*>(lo + o) = make_float4(rem(x.x), rem(x.y), rem(x.z), rem(x.w));
+    }
+  };
+
+  // ---- statistics chain state (thread 0 issues and publishes the window tiles)
+  const int chain_rank = chained ? int(blockIdx.x) % a.chain : 0;
+  float* const stage = Alo;  // [sa|sb][k][32 rows] of one window (kTcStatTile floats = both lo buffers)
+  uint32_t chain_pending = 0;  // thread 0: flag value to publish once the outstanding tile has landed
+  auto chain_release = [&]() {
+    if (chain_pending) {
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+      asm volatile("fence.proxy.async;" ::: "memory");
+      st_release_u32(a.chain_flags + blockIdx.x, chain_pending);
+      chain_pending = 0;
     }
   };
 
@@ -179,7 +224,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) solve_large_tc_kernel(const Sol
   const int fmb = min(tile0, 4 * FMB - 1) / 4;
   float acc[TPW][2][4];
   float vv[TPW][4];
-  auto phase_a = [&](int c) {
+  auto phase_a = [&](int c, auto fly_tag) {
+    constexpr bool kFly = decltype(fly_tag)::value;  // remainders of W from the hi copy on the fly
     const int c0 = c * kTcRows, rows = min(kTcRows, F - c0);
     const float* Wc = Ahi + (c & 1) * AW;
 #pragma unroll
@@ -211,6 +257,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) solve_large_tc_kernel(const Sol
     }
 #pragma unroll 1
     for (int q = 0; q < KB / 4; ++q) {
+      if (kFly && q == 2) chain_release();
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int kb = 4 * q + u, p = u & 1;
@@ -224,10 +271,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) solve_large_tc_kernel(const Sol
 #pragma unroll
         for (int i = 0; i < TPW; ++i) {
           const int o = 128 * q + xo[u];
-          bh[i][0] = __float_as_uint(wbase[i][o]);
-          bh[i][1] = __float_as_uint(wbase[i][o + 4]);
-          bl[i][0] = __float_as_uint(lbase[i][o]);
-          bl[i][1] = __float_as_uint(lbase[i][o + 4]);
+          const float w0 = wbase[i][o], w1 = wbase[i][o + 4];
+          bh[i][0] = __float_as_uint(w0);
+          bh[i][1] = __float_as_uint(w1);
+          bl[i][0] = __float_as_uint(kFly ? rem(w0) : lbase[i][o]);
+          bl[i][1] = __float_as_uint(kFly ? rem(w1) : lbase[i][o + 4]);
         }
 #pragma unroll
         for (int i = 0; i < TPW; ++i) mma_tf32(acc[i][p], al, bh[i][0], bh[i][1]);
@@ -269,12 +317,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) solve_large_tc_kernel(const Sol
     const bool stats_pass = pass == a.iters;
     const bool want_div = a.div_first ? pass == 0 : stats_pass;
     if (stats_pass) pdl_trigger();
+    lo_fly = stats_pass && chained;
     // prologue: windows 0 and 1 staged, phase A of window 0, B(0)
     fetch_w(0);
     store_w(0);
     if (nch > 1) fetch_w(1);
     __syncthreads();
-    phase_a(0);
+    if (lo_fly)
+      phase_a(0, std::true_type{});
+    else
+      phase_a(0, std::false_type{});
     phase_a_epilogue(0, want_div);
     if (nch > 1) {
       store_w(1);
@@ -364,25 +416,81 @@ __global__ void __launch_bounds__(kTcThreads, 1) solve_large_tc_kernel(const Sol
             }
           }
         }
-        const int FP = (F + 3) & ~3;
-        ISNMF_DASSERT(a.stats_cap == 0 || int(blockIdx.x) < a.stats_cap);
-        float* outA = a.stats + size_t(blockIdx.x) * 2 * FP * KP;
-        float* outB = outA + size_t(FP) * KP;
+        if (!chained) {
+          const int FP = (F + 3) & ~3;
+          ISNMF_DASSERT(a.stats_cap == 0 || int(blockIdx.x) < a.stats_cap);
+          float* outA = a.stats + size_t(blockIdx.x) * 2 * FP * KP;
+          float* outB = outA + size_t(FP) * KP;
 #pragma unroll
-        for (int rm = 0; rm < 2; ++rm)
+          for (int rm = 0; rm < 2; ++rm)
 #pragma unroll
-          for (int j = 0; j < KNW; ++j)
+            for (int j = 0; j < KNW; ++j)
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const int row = 16 * rm + g + 8 * (e >> 1), k = 8 * (warp * KNW + j) + 2 * t + (e & 1);
-              if (row < rows) {
-                outA[size_t(k) * FP + c0 + row] = sa[rm][j][e];
-                outB[size_t(k) * FP + c0 + row] = sb[rm][j][e];
+              for (int e = 0; e < 4; ++e) {
+                const int row = 16 * rm + g + 8 * (e >> 1), k = 8 * (warp * KNW + j) + 2 * t + (e & 1);
+                if (row < rows) {
+                  outA[size_t(k) * FP + c0 + row] = sa[rm][j][e];
+                  outB[size_t(k) * FP + c0 + row] = sb[rm][j][e];
+                }
               }
+        } else {
+          // the tile of window c - 1 has left the staging space (chain_release in phase A of this
+          // window, ahead of the barrier that ended the previous iteration)
+#pragma unroll
+          for (int rm = 0; rm < 2; ++rm)
+#pragma unroll
+            for (int j = 0; j < KNW; ++j)
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const int row = 16 * rm + g + 8 * (e >> 1), k = 8 * (warp * KNW + j) + 2 * t + (e & 1);
+                const int o = tc_stat_off(k, row);
+                stage[o] = sa[rm][j][e];  // rows past F carry exact zeros (q = r = 0 there)
+                stage[KP * kTcRows + o] = sb[rm][j][e];
+              }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncthreads();
+          if (tid == 0) {
+            const uint32_t target = a.chain_base + uint32_t(c) + 1u;
+            const int plane = int(blockIdx.x) / a.chain;
+            ISNMF_DASSERT(a.stats_cap == 0 || plane < a.stats_cap);
+            float* dst = a.stats + (size_t(plane) * nch + c) * kTcStatTile;
+            if (chain_rank > 0) {
+              const uint32_t* pf = a.chain_flags + blockIdx.x - 1;
+              int spins = 0;
+              while (int32_t(ld_acquire_u32(pf) - target) < 0)
+                if (++spins > kTcChainSpins) {
+                  atomicOr(a.status, ST_CHAIN_TIMEOUT);
+                  break;
+                }
+              asm volatile("fence.proxy.async;" ::: "memory");
             }
+            constexpr uint32_t kPiece = kTcStatTile * 4 / 4;  // four 16 KB copies
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const uint32_t src = smem_addr(stage) + i * kPiece;
+              const char* d = reinterpret_cast<const char*>(dst) + i * kPiece;
+              if (chain_rank == 0)
+                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(d), "r"(src),
+                             "r"(kPiece)
+                             : "memory");
+              else
+                asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(d),
+                             "r"(src), "r"(kPiece)
+                             : "memory");
+            }
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            chain_pending = target;
+          }
+        }
       }
       TC_STAMP(1, 0);
-      if (c + 1 < nch) phase_a(c + 1);  // on the warps while the tensor cores run window c
+      if (c + 1 < nch) {  // on the warps while the tensor cores run window c
+        if (lo_fly)
+          phase_a(c + 1, std::true_type{});
+        else
+          phase_a(c + 1, std::false_type{});
+      }
+      if (tid == 0) chain_release();     // (the last window's tile; otherwise done inside phase A)
       TC_STAMP(2, 32);
       if (!stats_pass) {
         mbar_wait(&mma_bar, mma_phase);  // window c's MMAs are done with A buffer c & 1 and B
@@ -439,6 +547,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) solve_large_tc_kernel(const Sol
     }
   }
 
+  if (chained && bad && tid == 0) st_release_u32(a.chain_flags + blockIdx.x, a.chain_base + kTcChainSpan - 1u);
   if (a.divpart && !bad) {
     double d = warp_sum_d(double(divacc));
     if (lane == 0) red[warp] = d;
