@@ -44,6 +44,10 @@ int pc_trace_set(unsigned long long* dev_ptr);
 using namespace isnmf_dev;
 
 namespace {
+#ifdef ISNMF_PHASE_PROF
+long long* g_work_prof = nullptr;  // K1M timeline of the batch / stateless passes (CTA 0, last tile)
+#endif
+
 
 thread_local std::string g_err;
 unsigned long long* g_trace_host = nullptr;  // isnmf_debug_pc_trace (ISNMF_PC_TRACE builds)
@@ -1351,6 +1355,18 @@ int isnmf_debug_phase_prof(isnmf_online* c, long long* out, int64_t cap, int32_t
   return 0;
 }
 
+// K1M stamps of CTA 0 in the batch / stateless passes (the last tile the CTA ran): [warp][64]
+int isnmf_debug_work_prof(long long* out, int64_t cap) {
+  const size_t n = 16 * 64;
+  if (!g_work_prof) {
+    CU(cudaMalloc(&g_work_prof, n * sizeof(long long)));
+    CU(cudaMemset(g_work_prof, 0, n * sizeof(long long)));
+  }
+  CU(cudaDeviceSynchronize());
+  if (out) CU(cudaMemcpy(out, g_work_prof, std::min<size_t>(n, size_t(cap)) * sizeof(long long), cudaMemcpyDeviceToHost));
+  return 0;
+}
+
 // per-CTA globaltimer stamps of the last fold_commit_kernel launch: [K*kFoldCluster][8]
 int isnmf_debug_fold_prof(isnmf_online* c, long long* out, int64_t cap) {
   const size_t n = size_t(c->K) * kFoldCluster * 8;
@@ -1610,6 +1626,9 @@ struct SolveWork {
       a.stats_cap = seg_blocks;
       a.status = &st->status;
       a.halt = halt_in ? halt_in : halt;
+#ifdef ISNMF_PHASE_PROF
+      a.prof = iters > 0 ? g_work_prof : nullptr;  // (not the final objective-only pass)
+#endif
       if (nblk > 0) {
         launch_solve(plan, nblk, a, s);
         launches++;

@@ -138,6 +138,39 @@ __device__ __forceinline__ void red_add(float* p, float v) {
   asm volatile("red.relaxed.gpu.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
 }
 
+// K1P exchange: st.async into the peer's shared memory with complete_tx on the peer's mbarrier
+// (no cluster barrier in the pass loop: barrier.cluster costs ~380 cycles and its acquire
+// invalidates L1, where the frames live; a release.cluster arrive costs a MEMBAR.ALL.GPU)
+__device__ __forceinline__ void mm_bar_init(unsigned long long* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(uint32_t(__cvta_generic_to_shared(bar))), "r"(count));
+}
+__device__ __forceinline__ uint32_t mm_peer_addr(const void* p, unsigned rank) {
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(uint32_t(__cvta_generic_to_shared(p))), "r"(rank));
+  return ra;
+}
+__device__ __forceinline__ void mm_st_async4(uint32_t raddr, float4 v, uint32_t rbar) {
+  asm volatile("st.async.weak.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+                   raddr),
+               "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void mm_bar_expect_tx(unsigned long long* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(uint32_t(__cvta_generic_to_shared(bar))),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mm_bar_wait(unsigned long long* bar, uint32_t parity) {
+  const uint32_t b = uint32_t(__cvta_generic_to_shared(bar));
+  uint32_t done = 0;
+  while (!done)
+    asm volatile(
+        "{\n\t.reg .pred P;\n\tmbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\tselp.b32 %0, 1, 0, P;\n\t}\n"
+        : "=r"(done)
+        : "r"(b), "r"(parity)
+        : "memory");
+}
+
 // One chunk of NBK 8-row blocks (rows row0 ...) of an iteration pass: phase A,
 // q/r in registers, phase B into nd[0] (num^T) / nd[1] (den^T).
 template <int KB, int WS, int NBK, bool DIV>
@@ -441,11 +474,17 @@ __global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a
   constexpr bool kCanPair = !MULTI && FG == 1;
   const bool pair2 = kCanPair && a.pair2 != 0;
   const unsigned crank = pair2 ? cluster_rank() : 0u;
+  // K1P: xbar[pass & 1] = the peer's row-half sums of that pass have landed in XR (transaction
+  // bytes of its st.async stores; a barrier is reused two passes later, behind our own next send)
+  __shared__ __align__(8) unsigned long long xbar[2];
   if constexpr (kCanPair) {
     if (pair2) {  // both CTAs take the same go decision (a status bit set meanwhile must not split them)
       __shared__ int s_go2[2];
       asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // the peer has started
       if (threadIdx.x == 0) {
+        mm_bar_init(&xbar[0], 1);
+        mm_bar_init(&xbar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;");
         const int go = !(*a.status || (a.halt && *a.halt));
         s_go2[crank] = go;
         *const_cast<int*>(map_rank(&s_go2[crank], crank ^ 1u)) = go;
@@ -509,6 +548,7 @@ __global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a
   float* Hstage = RED + ((KP * HT + 31) & ~31);
   for (int tile = tile0; tile < ntiles; tile += gridDim.x) {
   const bool first_tile = !MULTI || tile == int(blockIdx.x);
+  MM_STAMP(59);
   const bool staged = stage_next && !first_tile;
   const int n0 = tile * ntc;
   const int nf = min(ntc, a.nframes - n0);
@@ -683,10 +723,14 @@ __global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a
         }
       }
     } else if constexpr (kCanPair) {
-      // K1P: this CTA's row-half sums -> XR[pass & 1][rank] here and in the peer (DSMEM),
-      // cluster barrier, then rank 0 + rank 1 in that order in both CTAs.  Double-buffered by
-      // pass parity: the peer writes a buffer again two passes later, past the next barrier.
+      // K1P: this CTA's row-half sums -> XR[pass & 1][rank] here and in the peer (st.async over
+      // DSMEM, completing transaction bytes on the peer's xbar[pass & 1]); the thread that owns
+      // record p waits for the peer's records, then rank 0 + rank 1 in that order in both CTAs.
+      // Double-buffered by pass parity: the peer writes a buffer again two passes later, after
+      // every record of our pass between has reached it, each sent after its thread's reads here.
       float4* XR = reinterpret_cast<float4*>(RED + S::RED_FLOATS) + (pass & 1) * 2 * 2 * RECS;
+      if (gt == 0) mm_bar_expect_tx(&xbar[pass & 1], uint32_t(RECS * 2 * sizeof(float4)));
+      const uint32_t rbar = mm_peer_addr(&xbar[pass & 1], crank ^ 1u);
 #pragma unroll
       for (int m = 0; m < (RECS + RG * 32 - 1) / (RG * 32); ++m) {
         const int p = gt + m * RG * 32;
@@ -694,14 +738,14 @@ __global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a
           float4 num, den;
           rec_sum(p, num, den);
           float4* own = XR + (crank * RECS + p) * 2;
+          const uint32_t far = mm_peer_addr(own, crank ^ 1u);
+          mm_st_async4(far, num, rbar);
+          mm_st_async4(far + 16, den, rbar);
           own[0] = num;
           own[1] = den;
-          float4* far = const_cast<float4*>(map_rank(own, crank ^ 1u));
-          far[0] = num;
-          far[1] = den;
         }
       }
-      cluster_sync_all();
+      if (gt < RECS) mm_bar_wait(&xbar[pass & 1], uint32_t(pass >> 1) & 1u);
 #pragma unroll
       for (int m = 0; m < (RECS + RG * 32 - 1) / (RG * 32); ++m) {
         const int p = gt + m * RG * 32;
