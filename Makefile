@@ -54,5 +54,5 @@ $(TRC)/%.o: $(PKG)/csrc/%.cu $(DEPS)
 # experimental build with per-phase cycle counters (K1 headline variant only)
 prof: $(SRC) $(TABLES) $(DEPS)
 	@mkdir -p $(PKG)/lib_prof
-	$(NVCC) $(NVFLAGS) -DISNMF_PHASE_PROF -DISNMF_MIN_VARIANTS -shared -o $(PKG)/lib_prof/libisnmf_b200.so $(SRC) $(TABLES) -lcudart 2> $(PKG)/lib_prof/ptxas.log || (cat $(PKG)/lib_prof/ptxas.log; exit 1)
+	$(NVCC) $(NVFLAGS) $(EXTRA) -DISNMF_PHASE_PROF -DISNMF_MIN_VARIANTS -shared -o $(PKG)/lib_prof/libisnmf_b200.so $(SRC) $(TABLES) -lcudart 2> $(PKG)/lib_prof/ptxas.log || (cat $(PKG)/lib_prof/ptxas.log; exit 1)
 .PHONY: prof

@@ -803,7 +803,7 @@ int launch_block(isnmf_online* c, const float* dv, int64_t ldv, int nb, const ui
   const bool commit = (c->t_host + uint64_t(nb)) % uint64_t(c->beta) == 0;
   FoldArgs r = fold_args(c);
   r.nstat = chained ? (nblk + c->plan.chain - 1) / c->plan.chain : nblk;
-  r.stats_tiled = chained ? 1 : 0;
+  r.stats_tiled = chained ? 1 : c->plan.tiled ? 2 : 0;
   r.ndiv = (c->plan.pair || c->plan.mpair) ? 2 * nblk : nblk;
   r.nframes = nb;
   r.do_commit = commit;
@@ -1012,7 +1012,7 @@ int isnmf_online_create(isnmf_online** out, const isnmf_online_config* cfg) {
       (rc = dalloc(&c->B, FK)) || (rc = dalloc(&c->pa, FK)) || (rc = dalloc(&c->pb, FK)) ||
       (rc = dalloc(&c->cta_part, size_t(fold_parts(c->K)))) ||
       (rc = dalloc(&c->W32, size_t(c->F) * c->WS)) ||
-      (rc = dalloc(&c->stats, size_t(c->maxblk) * 2 * padded_f(c->F) * c->KP + 4)) ||
+      (rc = dalloc(&c->stats, size_t(c->maxblk) * 2 * ((c->F + 15) & ~int64_t(15)) * c->KP + 4)) ||
       (rc = dalloc(&c->divpart, 2 * size_t(c->maxblk))) ||
       (c->plan.chain > 1 && (rc = dalloc(&c->chain_flags, size_t(c->maxblk)))) ||
       (c->plan.pair && (rc = dalloc(&c->WB, size_t(2) * 2 * c->KP * kWbRows))) ||
@@ -1564,7 +1564,7 @@ struct SolveWork {
     TRY(dalloc(&cta_part, size_t(fold_parts(K))));
     TRY(dalloc(&P, 2 * size_t(K)));
     TRY(dalloc(&scale, size_t(K)));
-    TRY(dalloc(&stats, size_t(seg_blocks) * 2 * padded_f(F) * KP + 4));
+    TRY(dalloc(&stats, size_t(seg_blocks) * 2 * ((F + 15) & ~int64_t(15)) * KP + 4));
     TRY(dalloc(&divpart, size_t(seg_blocks)));
     TRY(dalloc(&halt, 1));
     CU(cudaMemset(halt, 0, sizeof(unsigned int)));
@@ -1636,6 +1636,7 @@ struct SolveWork {
       FoldArgs r = fold_args();
       r.halt = halt_in ? const_cast<unsigned int*>(halt_in) : halt;
       r.nstat = stats_on ? nblk : 0;
+      r.stats_tiled = plan.tiled ? 2 : 0;
       r.ndiv = nblk;
       r.nframes = int(ns);
       r.do_commit = commit && s0 + seg >= n;

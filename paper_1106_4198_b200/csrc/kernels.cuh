@@ -1029,7 +1029,8 @@ struct FoldArgs {
   double* scale_out;  // optional: column scales s_k of this commit (batch H compensation)
   int batch_mode;
   int stats_cap;      // planes / divergence partials allocated (debug checks; 0 = unchecked)
-  int stats_tiled;    // planes in K1T's chained layout: [window of 32 rows][sa|sb][KP][32], rows swizzled by k
+  int stats_tiled;    // 1: K1T's chained layout [window of 32 rows][sa|sb][KP][32], rows swizzled by k; 2: K1M's
+                      // [window of 16 rows][sa|sb][K][16] (kernels_mma.cuh mm_plane_off)
   long long p_cap;    // rows of P (debug checks; 0 = unchecked)
   long long* tprof;  // ISNMF_PHASE_PROF builds: [gridDim][8] globaltimer stamps of thread 0
 };
@@ -1144,13 +1145,19 @@ __global__ void __cluster_dims__(kFoldCluster, 1, 1) __launch_bounds__(kFoldThre
   const size_t plane = size_t(FP) * a.KP;
   const int b0 = int((long long)r * a.nstat / kFoldCluster), b1 = int((long long)(r + 1) * a.nstat / kFoldCluster);
   // plane geometry: [sa|sb][KP][FP], or K1T's chained window tiles (kernels_large_tc.cuh tc_stat_off)
-  const size_t pstride = a.stats_tiled ? size_t((F + 31) / 32) * 2 * a.KP * 32 : 2 * plane;
-  const size_t yoff = a.stats_tiled ? size_t(a.KP) * 32 : plane;
+  // or K1M's windows of 16 rows [window][sa|sb][K][16] (stats_tiled = 2, kernels_mma.cuh mm_plane_off)
+  const size_t pstride = a.stats_tiled == 2   ? size_t((F + 15) / 16) * 2 * a.K * 16
+                         : a.stats_tiled == 1 ? size_t((F + 31) / 32) * 2 * a.KP * 32
+                                              : 2 * plane;
+  const size_t yoff = a.stats_tiled == 2 ? size_t(a.K) * 16 : a.stats_tiled == 1 ? size_t(a.KP) * 32 : plane;
   for (int it = tid; it < NQ * G; it += kFoldThreads) {
     const int q = it % NQ, g = it / NQ;
-    const float* base = a.stats_tiled ? a.stats + size_t(q >> 3) * 2 * a.KP * 32 + size_t(k) * 32 +
-                                            ((4 * (q & 7)) ^ (((k >> 1) & 3) << 3))
-                                      : a.stats + size_t(k) * FP + 4 * q;
+    const float* base =
+        a.stats_tiled == 2   ? a.stats + size_t(q >> 2) * 2 * a.K * 16 + size_t(k) * 16 +
+                                   ((4 * (q & 3)) ^ (((k >> 1) & 1) << 3))
+        : a.stats_tiled == 1 ? a.stats + size_t(q >> 3) * 2 * a.KP * 32 + size_t(k) * 32 +
+                                   ((4 * (q & 7)) ^ (((k >> 1) & 3) << 3))
+                             : a.stats + size_t(k) * FP + 4 * q;
     double s[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
 #pragma unroll 4
     for (int b = b0 + g; b < b1; b += G) {

@@ -134,9 +134,11 @@ __device__ __forceinline__ void put_hf(float* p, float h) {
 }
 
 __device__ __forceinline__ float2 lds64(const float* p) { return *reinterpret_cast<const float2*>(p); }
-__device__ __forceinline__ void red_add(float* p, float v) {
-  asm volatile("red.relaxed.gpu.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
-}
+// K1M statistics planes: [window of 16 rows][sa | sb][K][16 rows], the rows of a [K][16] tile
+// XOR-swizzled by k (2-way instead of 4-way bank conflicts when the C fragments are staged);
+// K2 (fold_commit_kernel, stats_tiled = 2) reads float4 row quads of one k
+__host__ __device__ __forceinline__ size_t mm_plane_floats(int F, int K) { return size_t((F + 15) >> 4) * 2 * K * 16; }
+__host__ __device__ __forceinline__ int mm_plane_off(int k, int row16) { return k * 16 + (row16 ^ (((k >> 1) & 1) << 3)); }
 
 // K1P exchange: st.async into the peer's shared memory with complete_tx on the peer's mbarrier
 // (no cluster barrier in the pass loop: barrier.cluster costs ~380 cycles and its acquire
@@ -308,7 +310,7 @@ __device__ __forceinline__ void mm_stats_block(const float* Ws, const float* Hf,
                                                const float* const* fptr, int f0, int F, int nf, float eps, int g,
                                                int t, bool want_div, float& divacc, float* outA, float* outB, int FP,
                                                float (&vv)[2 * FG][4], int f0n, long long* prof, int ev,
-                                               bool accumulate) {
+                                               bool accumulate, int K, float* stg, bool first_block) {
   constexpr int NB = 2 * FG;  // frame blocks of 8
   MM_STAMP_P(prof, ev);
   float acc[NB][4];
@@ -407,49 +409,56 @@ __device__ __forceinline__ void mm_stats_block(const float* Ws, const float* Hf,
     }
   }
   MM_STAMP_P(prof, ev + 3);
-  // planes are [KP][FP]: rows k >= K hold zeros (h = 0 there), so only f is guarded
-  float* pa = outA + size_t(2 * t) * FP + f0 + g;
-  float* pb = outB + size_t(2 * t) * FP + f0 + g;
-  const bool ok0 = f0 + g < F, ok1 = f0 + g + 8 < F;
+#ifdef ISNMF_SKIP_STATS_STORE  // timing-only builds: the cost of the plane stores / reductions
+  if (sa[0][0] != 12345.678f) return;
+#endif
+  // The block's [sa | sb] leave as two TMA bulk copies of one [K][16 rows] tile each (plane
+  // layout mm_plane_off below): 56 scattered 4-byte stores / reductions per lane cost ~4.5k
+  // cycles per block at config 2 (one 32-byte sector request each), a bulk copy moves whole
+  // lines.  The warp's staging tile is reused for sa, then sb: its previous copy must have
+  // read it (wait_group.read).  A CTA that owns several frame tiles (batch) adds into its
+  // plane with cp.reduce.async.bulk add.f32 after the first; every cell has one issuing
+  // thread (lane 0 of the warp that owns the block in every tile) and that thread waits for
+  // its previous tile's copies to complete before the first of this tile (first_block), so
+  // the sums are formed in tile order: deterministic, bitwise reproducible.
+  const int K16 = K * 16;
+  float* gA = outA + size_t(f0 >> 4) * 2 * K16;  // outA = the plane; the window's sa tile, sb behind it
 #pragma unroll
-  if (!accumulate) {
+  for (int ab = 0; ab < 2; ++ab) {
+    if ((g | t) == 0) {
+      if (ab == 0 && first_block)
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+      else
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    }
+    __syncwarp();
 #pragma unroll
     for (int j = 0; j < KB; ++j) {
-      const size_t o = size_t(8 * j) * FP;
-      if (ok0) {
-        pa[o] = sa[j][0];
-        pa[o + FP] = sa[j][1];
-        pb[o] = sb[j][0];
-        pb[o + FP] = sb[j][1];
+      const int k0 = 8 * j + 2 * t, sw = (t & 1) << 3;  // ((k >> 1) & 1) << 3 for k0 and k0 + 1
+      const float(&v)[4] = ab ? sb[j] : sa[j];
+      if (k0 < K) {
+        stg[k0 * 16 + (g ^ sw)] = v[0];
+        stg[k0 * 16 + ((g + 8) ^ sw)] = v[2];
       }
-      if (ok1) {
-        pa[o + 8] = sa[j][2];
-        pa[o + FP + 8] = sa[j][3];
-        pb[o + 8] = sb[j][2];
-        pb[o + FP + 8] = sb[j][3];
+      if (k0 + 1 < K) {
+        stg[(k0 + 1) * 16 + (g ^ sw)] = v[1];
+        stg[(k0 + 1) * 16 + ((g + 8) ^ sw)] = v[3];
       }
     }
-    return;
-  }
-  // A CTA that owns several frame tiles (batch) adds into its planes after the first
-  // with fire-and-forget reductions (red.global.add: no load round trip on the
-  // critical path).  The planes are private to the CTA and every cell has one writer
-  // thread, whose same-address operations are ordered (per-location coherence), so the
-  // sums are formed in tile order: deterministic, bitwise reproducible.
-#pragma unroll
-  for (int j = 0; j < KB; ++j) {
-    const size_t o = size_t(8 * j) * FP;
-    if (ok0) {
-      red_add(pa + o, sa[j][0]);
-      red_add(pa + o + FP, sa[j][1]);
-      red_add(pb + o, sb[j][0]);
-      red_add(pb + o + FP, sb[j][1]);
-    }
-    if (ok1) {
-      red_add(pa + o + 8, sa[j][2]);
-      red_add(pa + o + FP + 8, sa[j][3]);
-      red_add(pb + o + 8, sb[j][2]);
-      red_add(pb + o + FP + 8, sb[j][3]);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if ((g | t) == 0) {
+      const uint32_t src = static_cast<uint32_t>(__cvta_generic_to_shared(stg));
+      float* dst = gA + ab * K16;
+      const uint32_t bytes = uint32_t(K16) * 4u;
+      if (accumulate)
+        asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(dst), "r"(src),
+                     "r"(bytes)
+                     : "memory");
+      else
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src), "r"(bytes)
+                     : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     }
   }
 }
@@ -783,19 +792,28 @@ __global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a
         asm volatile("prefetch.global.L2 [%0];" ::"l"(v1 + off));
     }
     __syncthreads();
-    const int FP = (F + 3) & ~3;
     // (K1P: the pair's plane, this CTA's rows)
     ISNMF_DASSERT(!a.stats || a.stats_cap == 0 || (pair2 ? tile : int(blockIdx.x)) < a.stats_cap);
-    float* outA = a.stats ? a.stats + size_t(pair2 ? tile : int(blockIdx.x)) * 2 * FP * KP : nullptr;
-    float* outB = a.stats ? outA + size_t(FP) * KP : nullptr;
+    float* plane = a.stats ? a.stats + size_t(pair2 ? tile : int(blockIdx.x)) * mm_plane_floats(F, K) : nullptr;
+    // this warp's staging tile [K][16] (behind h^T and the next tile's staged H0 in RED)
+    float* stg = Hstage + ((NT * KP + 31) & ~31) + warp * 16 * KP;
     float vv[2 * FG][4];
     if (M0 + warp < M1) mm_stats_v<2 * FG>(vv, fptr, 16 * (M0 + warp), F, nf, g, t);
 #pragma unroll 1
     for (int m = M0 + warp; m < M1; m += kMmThreads / 32) {
       const int mn = m + kMmThreads / 32;
-      mm_stats_block<KB, FG, WS, HT>(Ws, Hf, Ht, fptr, 16 * m, F, nf, eps, g, t, want_div, divacc, outA, outB,
-                                         FP, vv, mn < M1 ? 16 * mn : -1, a.prof,
-                                         44 + 4 * ((m - M0 - warp) / (kMmThreads / 32)), !first_tile);
+      mm_stats_block<KB, FG, WS, HT>(Ws, Hf, Ht, fptr, 16 * m, F, nf, eps, g, t, want_div, divacc, plane, plane,
+                                         0, vv, mn < M1 ? 16 * mn : -1, a.prof,
+                                         44 + 4 * ((m - M0 - warp) / (kMmThreads / 32)), !first_tile, K, stg,
+                                         m == M0 + warp);
+    }
+    // the staging tiles lie in RED: the copies must have read them before the next tile's
+    // partials (or the CTA's exit) — and have completed before the grid ends
+    if (plane && lane == 0) {
+      if (MULTI && tile + int(gridDim.x) < ntiles)
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      else
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
   }
   divd += double(divacc);

@@ -45,6 +45,12 @@ for w in range(nw):
         prev = e[3]
     print(f"{w:3d} {r[0] - t0:8d}  " + "  ".join(parts[:3]) + f"  ...  {r[61] - r[60]:6d}  {r[61] - t0:7d}")
 tot /= nw * iters
+print("per pass (mean over warps / max over warps): mma, bar1, update, bar2")
+for p in range(iters):
+    prev = ts[:, 4 * p] if p else ts[:, 0]
+    e = [ts[:, 1 + 4 * p], ts[:, 2 + 4 * p], ts[:, 3 + 4 * p], ts[:, 4 + 4 * p]]
+    d = [e[0] - prev, e[1] - e[0], e[2] - e[1], e[3] - e[2]]
+    print(f"  pass {p}: " + "  ".join(f"{int(x.mean())}/{int(x.max())}" for x in d) + f"   pass total {int((e[3] - prev).max())}")
 print("mean per pass: mma %.0f  bar1 %.0f  update %.0f  bar2 %.0f" % tuple(tot))
 print("statistics blocks (cycles): phaseA' / q,r,div / stats MMAs / stores")
 for w in range(nw):
