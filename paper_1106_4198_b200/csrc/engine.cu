@@ -208,6 +208,17 @@ int launch_fold(const FoldArgs& f, cudaStream_t s, bool pdl = false) {
   return 0;
 }
 int fold_parts(int K) { return 2 * K * kFoldCluster; }
+// Divisor of the shrinking tail of the host-frame chunk schedule (online_enqueue): 8 for
+// shapes whose copy and compute are balanced, 4 for compute-bound ones.  ISNMF_TAIL overrides.
+int tail_div(int K, int iters) {
+  static const int env = [] {
+    const char* e = getenv("ISNMF_TAIL");
+    return e ? atoi(e) : 0;
+  }();
+  if (env > 1) return env;
+  return ramp_factor(K, iters) <= 1.5 ? 8 : 4;
+}
+
 int padded_f(int F) { return (F + 3) & ~3; }
 
 // Picks the variant for (F, K, frames per mini-batch).
@@ -904,11 +915,15 @@ int online_enqueue(isnmf_online* c, const float* frames, int64_t ldv, int64_t n,
   double ramp = double(c->beta);
   while (pos < n_eff) {
     const int64_t rb = std::max<int64_t>(int64_t(c->beta), int64_t(ramp / c->beta) * c->beta);
-    // ... and shrink towards the end (at most a quarter of what is left, whole mini-batches):
+    // ... and shrink towards the end (a fraction of what is left, whole mini-batches):
     // the last chunk's compute (copy-bound shapes) or copy (compute-bound ones) is not
-    // overlapped, so it must be short — a 64-mini-batch last chunk cost 8 ms per config-3 pass
+    // overlapped, so it must be short — a 64-mini-batch last chunk cost 8 ms per config-3 pass.
+    // With two buffers the copy of chunk i+1 waits for the compute of chunk i-1, which runs
+    // beside the copy of chunk i: when copy and compute are balanced (config 3 with K1C:
+    // compute = 0.82 x copy per frame) a chunk must not be much shorter than its predecessor or
+    // the copy engine idles — quarters (ratio 0.75) cost ~2.5 ms per pass, eighths (0.875) do not.
     const int64_t rem = n_eff - pos;
-    const int64_t tail = std::max<int64_t>(int64_t(c->beta), (rem / 4) / c->beta * c->beta);
+    const int64_t tail = std::max<int64_t>(int64_t(c->beta), (rem / tail_div(c->K, c->iters)) / c->beta * c->beta);
     const int64_t cf = std::min<int64_t>(std::min<int64_t>(std::min<int64_t>(c->chunk, rb), tail), rem);
     ramp *= ramp_factor(c->K, c->iters);
     CU(cudaStreamWaitEvent(c->xs, c->ev_free[buf], 0));
