@@ -34,6 +34,26 @@ def test_batch_matches_oracle(F, K, N, epochs):
     assert np.all(np.diff(np.concatenate([[got["initial_obj"]], got["obj"]])) <= 1e-6 * got["initial_obj"])
 
 
+def test_batch_multi_tile_ctas_match_oracle_and_reproduce():
+    """N large enough that every CTA of the persistent K1M launch owns several frame tiles
+    (148 CTAs x 32 frames per tile): the CTA's statistics plane is written by a bulk store for
+    its first tile and accumulated by cp.reduce.async.bulk adds for the others, in tile order —
+    per-epoch objectives and W against the oracle, and two runs bitwise identical."""
+    F, K, N, epochs = 100, 20, 3 * 148 * 32 + 1234, 3  # 3-4 tiles per CTA, ragged last tile
+    v = spectrogram_np(F, K, N, seed=31)
+    rng = np.random.default_rng(32)
+    w0 = rng.uniform(0.1, 1.0, size=(F, K))
+    h0 = rng.uniform(0.1, 1.0, size=(K, N))
+    got = E.batch_train(v, w0, h0, epochs)
+    ref = O.batch_train(v.astype(np.float64), w0, h0, epochs)
+    assert rel(got["initial_obj"], ref["initial_obj"]) < RTOL
+    assert rel(got["obj"], ref["obj"]) < RTOL
+    assert rel(got["w"], ref["w"]) < 1e-3
+    again = E.batch_train(v, w0, h0, epochs)
+    assert np.array_equal(got["w"], again["w"]) and np.array_equal(got["obj"], again["obj"])
+    assert np.array_equal(got["h"], again["h"])
+
+
 def test_batch_eta_stop_and_final_objective():
     F, K, N = 64, 4, 500
     v = spectrogram_np(F, K, N, seed=5)
