@@ -211,6 +211,17 @@ __device__ __forceinline__ int64_t warm_col(const SolveArgs& a, int n) {  // n =
   ISNMF_DASSERT(col >= 0 && col < a.wmod);
   return col;
 }
+// L2 prefetch of the tag and the U row of launch-local frame n: safe before the PDL wait (L2 is
+// the coherence point: a later load sees whatever a launch still in flight writes), and it turns
+// the two dependent HBM round trips of the prologue (tag, then U) into L2 hits
+__device__ __forceinline__ void warm_prefetch(const SolveArgs& a, int n) {
+  const int64_t col = warm_col(a, n);
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(a.T + col));
+  const char* u = reinterpret_cast<const char*>(a.U + size_t(col) * a.K);
+  const int bytes = a.K * int(sizeof(double));
+  for (int off = 0; off < bytes + 127; off += 128)
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(u + (off < bytes ? off : bytes - 1)));
+}
 __device__ __forceinline__ double warm_value(const SolveArgs& a, int64_t col, uint32_t tag, int k) {
   ISNMF_DASSERT(tag <= a.c_now && k >= 0 && k < a.K);
   return a.U[size_t(col) * a.K + k] * (a.P[size_t(a.c_now) * a.K + k] / a.P[size_t(tag) * a.K + k]);

@@ -474,6 +474,13 @@ __global__ void __launch_bounds__(32 * NW, 1) solve_mma_kernel(const SolveArgs a
   MM_STAMP(62);
   if constexpr (!MULTI && FG == 1)
     if (a.pair2) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");  // (waited below)
+  if constexpr (!MULTI) {  // warm-store lines of this CTA's frames towards L2, beside the previous K2
+    if (a.h0_mode == 1) {
+      const int t0 = (FG == 1 && a.pair2) ? int(blockIdx.x >> 1) : int(blockIdx.x);
+      const int nfr = min(a.cta_frames, a.nframes - t0 * a.cta_frames);
+      if (int(threadIdx.x) < nfr) warm_prefetch(a, t0 * a.cta_frames + int(threadIdx.x));
+    }
+  }
   pdl_wait();
   MM_STAMP(58);
   // K1P (a.pair2; online, one frame group): a 2-CTA cluster shares the tile's frames, rank r

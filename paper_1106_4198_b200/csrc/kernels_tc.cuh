@@ -332,6 +332,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPcThreads, 1) solve
       vr[t][j] = (row < rowF && n < nf ? __ldg(fptr[n] + row) : 0.0f) + eps;
     }
   }
+  if (a.h0_mode == 1 && tid < nf) warm_prefetch(a, n0 + tid);
   pdl_wait();
   PC_MARK(20, 0);
   if (tid == 0) {
