@@ -1114,7 +1114,7 @@ __global__ void __cluster_dims__(kFoldCluster, 1, 1) __launch_bounds__(kFoldThre
   pdl_trigger();  // the next K1 may start its launch; it waits for this grid before touching its outputs
   extern __shared__ __align__(16) double fsm[];
   __shared__ double red[kFoldWarps];
-  __shared__ double s_cs, s_sc;
+  __shared__ double s_csr[kFoldCluster];
   __shared__ int s_last;
   const int F = a.F, tid = threadIdx.x;
   FOLD_T(0);
@@ -1265,17 +1265,16 @@ __global__ void __cluster_dims__(kFoldCluster, 1, 1) __launch_bounds__(kFoldThre
   if (bad) atomicOr(&a.st->pad, bad);
   FOLD_T(3);
   cs = block_sum_d(cs, red);
-  if (tid == 0) s_cs = cs;
+  // ---- 3. column scale s_k, rescale of this rank's rows: every rank pushes its partial into
+  // all four CTAs (DSMEM stores), one cluster barrier, then the same rank-order sum everywhere
+  // (no rank touches another's shared memory after the barrier)
+  if (tid == 0)
+    for (int i = 0; i < kFoldCluster; ++i) *const_cast<double*>(map_rank(&s_csr[r], unsigned(i))) = cs;
   cluster_sync_all();
   FOLD_T(4);
-  // ---- 3. column scale s_k (rank order), rescale of this rank's rows
-  if (tid == 0) {
-    double sc = 0.0;
-    for (int i = 0; i < kFoldCluster; ++i) sc += *map_rank(&s_cs, unsigned(i));
-    s_sc = sc;
-  }
-  cluster_sync_all();  // s_sc visible; no rank reads another's shared memory after this
-  const double sc = s_sc;
+  double sc = 0.0;
+#pragma unroll
+  for (int i = 0; i < kFoldCluster; ++i) sc += s_csr[i];
   const bool ok = sc > 0.0;
   double d2 = 0.0, cw = 0.0;
   for (int f = lo + tid; f < hi; f += kFoldThreads) {
