@@ -1108,12 +1108,33 @@ __device__ __forceinline__ double block_sum_d(double v, double* red) {
   return s;
 }
 
+// two values at once (same per-value order as block_sum_d; red holds 2 * kFoldWarps doubles)
+__device__ __forceinline__ void block_sum2_d(double& x, double& y, double* red) {
+  x = warp_sum_d(x);
+  y = warp_sum_d(y);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) {
+    red[warp] = x;
+    red[kFoldWarps + warp] = y;
+  }
+  __syncthreads();
+  double sx = 0.0, sy = 0.0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < kFoldWarps; ++w) {
+      sx += red[w];
+      sy += red[kFoldWarps + w];
+    }
+  x = sx;
+  y = sy;
+}
+
 #ifndef ISNMF_TEMPLATES_ONLY  // defined once, in engine.cu's translation unit
 __global__ void __cluster_dims__(kFoldCluster, 1, 1) __launch_bounds__(kFoldThreads)
     fold_commit_kernel(const FoldArgs a) {
   pdl_trigger();  // the next K1 may start its launch; it waits for this grid before touching its outputs
   extern __shared__ __align__(16) double fsm[];
-  __shared__ double red[kFoldWarps];
+  __shared__ double red[2 * kFoldWarps];
   __shared__ double s_csr[kFoldCluster];
   __shared__ int s_last;
   const int F = a.F, tid = threadIdx.x;
@@ -1307,8 +1328,7 @@ __global__ void __cluster_dims__(kFoldCluster, 1, 1) __launch_bounds__(kFoldThre
   }
   if (!ok && tid == 0) atomicOr(&a.st->pad, ST_ZERO_COLUMN);
   FOLD_T(5);
-  d2 = block_sum_d(d2, red);
-  cw = block_sum_d(cw, red);
+  block_sum2_d(d2, cw, red);
   if (tid == 0) {
     a.cta_part[2 * blockIdx.x] = d2;
     a.cta_part[2 * blockIdx.x + 1] = cw;
@@ -1325,8 +1345,7 @@ __global__ void __cluster_dims__(kFoldCluster, 1, 1) __launch_bounds__(kFoldThre
     pd += __ldcg(a.cta_part + 2 * b);
     pw += __ldcg(a.cta_part + 2 * b + 1);
   }
-  pd = block_sum_d(pd, red);
-  pw = block_sum_d(pw, red);
+  block_sum2_d(pd, pw, red);
   if (tid == 0) {
     volatile DevState* st = a.st;
     const unsigned int err = st->pad;
