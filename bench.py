@@ -289,7 +289,7 @@ def run_batch(args, rank, world):
     vd = spectrogram_torch(F, K, N, seed=7 + rank, shape=cfg["shape"], device="cuda")
     rng = np.random.default_rng(8 + rank)
     w0 = rng.uniform(0.1, 1.0, size=(F, K))
-    h0 = rng.uniform(0.1, 1.0, size=(K, N))
+    h0 = np.asfortranarray(rng.uniform(0.1, 1.0, size=(K, N)))  # column-major, as the C ABI takes it
     torch.cuda.synchronize()
     E.batch_profile(1)
     for _ in range(max(1, args.warmup)):

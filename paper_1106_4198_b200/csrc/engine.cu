@@ -561,6 +561,21 @@ __global__ void fill_f64(double* p, int64_t n, double v) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
     p[i] = v;
 }
+// batch_train's H: fp64 (host layout) <-> the solver's fp32, on the device; *bad is set when
+// an entry is not strictly positive (NonPositiveInit)
+__global__ void h_to_f32(const double* src, float* dst, int64_t n, unsigned int* bad) {
+  unsigned int b = 0;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const double x = src[i];
+    if (!(x > 0.0)) b = 1;
+    dst[i] = float(x);
+  }
+  if (b) atomicOr(bad, 1u);
+}
+__global__ void h_to_f64(const float* src, double* dst, int64_t n) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    dst[i] = double(src[i]);
+}
 // U[col] <- current value (U * P[c]/P[T]), T <- c_new.
 __global__ void warm_rebase(double* U, uint32_t* T, const double* P, int64_t n, int K, uint32_t c_old,
                             uint32_t c_new) {
@@ -1872,26 +1887,43 @@ int isnmf_batch_train(const float* v, int64_t ldv, int64_t F, int64_t N, int64_t
   if (!(eps > 0.0)) return fail(ISNMF_E_NEGATIVE_INPUT, "config: epsilon must be > 0");
   for (int64_t i = 0; i < F * K; ++i)
     if (!(w0[i] > 0.0)) return fail(ISNMF_E_NON_POSITIVE_INIT, "batch_train: w0 and h0 must be strictly positive");
-  for (int64_t i = 0; i < K * N; ++i)
-    if (!(h0[i] > 0.0)) return fail(ISNMF_E_NON_POSITIVE_INIT, "batch_train: w0 and h0 must be strictly positive");
   SolveWork wk;
   TRY(wk.init(F, K, N));
   TRY(wk.set_w(w0));
-  DevBuf bv, bh;
+  DevBuf bv, bh, bh64;
   const float* dv = v;
   int64_t dld = ldv;
   if (!is_device_ptr(v)) {
     float* tmp = nullptr;
     TRY(dalloc(&tmp, size_t(F) * N));
-    CU(cudaMemcpy2D(tmp, size_t(F) * sizeof(float), v, size_t(ldv) * sizeof(float), size_t(F) * sizeof(float),
-                    size_t(N), cudaMemcpyHostToDevice));
+    if (ldv == F)  // contiguous frames: one linear DMA (2D copies run far below PCIe speed)
+      CU(cudaMemcpy(tmp, v, size_t(F) * N * sizeof(float), cudaMemcpyHostToDevice));
+    else
+      CU(cudaMemcpy2D(tmp, size_t(F) * sizeof(float), v, size_t(ldv) * sizeof(float), size_t(F) * sizeof(float),
+                      size_t(N), cudaMemcpyHostToDevice));
     bv.p = tmp;
     dv = tmp;
     dld = F;
   }
+  // H0 goes up as the caller's fp64 and is converted (and checked: h0 > 0) on the device; the
+  // same fp64 buffer takes the final H back
   float* dh = nullptr;
-  TRY(upload_h(h0, K, N, &dh));
+  double* dh64 = nullptr;
+  TRY(dalloc(&dh, size_t(K) * N));
   bh.p = dh;
+  TRY(dalloc(&dh64, size_t(K) * N));
+  bh64.p = dh64;
+  CU(cudaMemcpy(dh64, h0, size_t(K) * N * sizeof(double), cudaMemcpyHostToDevice));
+  TRY(settle());  // (pageable copies return once staged: the DMAs of V and H0 must have landed)
+  CU(cudaMemsetAsync(wk.halt, 0, sizeof(unsigned int), wk.s));
+  h_to_f32<<<1184, 256, 0, wk.s>>>(dh64, dh, K * N, wk.halt);
+  {
+    unsigned int bad = 0;
+    CU(cudaMemcpyAsync(&bad, wk.halt, sizeof(bad), cudaMemcpyDeviceToHost, wk.s));
+    CU(cudaMemsetAsync(wk.halt, 0, sizeof(unsigned int), wk.s));
+    CU(cudaStreamSynchronize(wk.s));
+    if (bad) return fail(ISNMF_E_NON_POSITIVE_INIT, "batch_train: w0 and h0 must be strictly positive");
+  }
   // the column scales of the last commit multiply H on its next read (rescale_dictionary's
   // H compensation, model.hpp:84, applied lazily)
   fill_f64<<<1, 256, 0, wk.s>>>(wk.scale, K, 1.0);
@@ -1942,9 +1974,9 @@ int isnmf_batch_train(const float* v, int64_t ldv, int64_t F, int64_t N, int64_t
     *initial_obj = obj;
   }
   CU(cudaMemcpy(w_out, wk.W64, size_t(F) * K * sizeof(double), cudaMemcpyDeviceToHost));
-  std::vector<float> h32(size_t(K) * N);
-  CU(cudaMemcpy(h32.data(), dh, h32.size() * sizeof(float), cudaMemcpyDeviceToHost));
-  for (size_t i = 0; i < h32.size(); ++i) h_out[i] = h32[i];
+  h_to_f64<<<1184, 256, 0, wk.s>>>(dh, dh64, K * N);
+  CU(cudaStreamSynchronize(wk.s));
+  CU(cudaMemcpy(h_out, dh64, size_t(K) * N * sizeof(double), cudaMemcpyDeviceToHost));
   if (epochs) *epochs = done;
   if (last_delta) *last_delta = delta;
   if (g_prof.on) {
