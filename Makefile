@@ -48,7 +48,7 @@ $(TRC)/libisnmf_b200.so: $(OBJ:$(PKG)/lib/%.o=$(TRC)/%.o)
 	$(NVCC) $(ARCH) -shared -o $@ $^ -lcudart
 $(TRC)/%.o: $(PKG)/csrc/%.cu $(DEPS)
 	@mkdir -p $(TRC)
-	$(NVCC) $(NVFLAGS) -DISNMF_PC_TRACE -c -o $@ $< 2> $(TRC)/$*.ptxas.log || (cat $(TRC)/$*.ptxas.log; exit 1)
+	$(NVCC) $(NVFLAGS) $(EXTRA) -DISNMF_PC_TRACE -c -o $@ $< 2> $(TRC)/$*.ptxas.log || (cat $(TRC)/$*.ptxas.log; exit 1)
 .PHONY: trace
 
 # experimental build with per-phase cycle counters (K1 headline variant only)
