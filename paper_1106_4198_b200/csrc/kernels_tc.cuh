@@ -230,7 +230,7 @@ static __device__ unsigned long long* g_pc_trace = nullptr;  // (tc_table.cu's c
 // per-warp timeline of CTAs 0 and 1 in shared memory (a store to sysmem before a
 // barrier.cluster.arrive.release would be waited for), dumped at the end of the launch to
 // g_pc_trace[4096 + (cta * 10 + warp) * 512 ..]: clock64 << 16 | site << 8 | (arg & 0xff)
-constexpr int kPcLog = 96;
+constexpr int kPcLog = 128;
 #ifndef ISNMF_PC_TRACE_MIN
 #define ISNMF_PC_TRACE_MIN 0  // 7: pass-level sites only (the whole launch fits the log)
 #endif
@@ -616,20 +616,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPcThreads, 1) solve
     if (stats_pass) {
       // h^T (hi | lo rows) for the statistics B operand, built while phase A runs; the slots are
       // free (the last update read the exchange buffer before the end-of-pass barrier)
-      for (int idx = tid; idx < S::HT_ROWS * (kPcFrames / 4); idx += kPcThreads) {
-        const int kp = idx / (kPcFrames / 4), n4 = 4 * (idx - kp * (kPcFrames / 4));
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (kp < KP2) {
-          const int k = kp < KP ? kp : kp - KP;
+      // item = (atom k = 8a + it % 8, frames 4jj ..): a quarter warp writes the 8 rows of one
+      // core-matrix group (conflict-free float4 stores), its h reads are 4-way conflicted scalar
+      // loads (the earlier row-major walk was 8- to 16-way conflicted on both sides, ~4k cycles)
+      static_assert(S::HT_ROWS == KP2 + 8 && kPcFrames == 64, "h^T item map");
+      for (int it = tid; it < (KP + 8) * (kPcFrames / 4); it += kPcThreads) {
+        const int t8 = it & 7, jj = (it >> 3) & 15, k = ((it >> 7) << 3) + t8;
+        if (k < KP) {
           float x[4];
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float h = Hh[pc_off_h<KP>(n4 + e, k)];
-            x[e] = kp < KP ? h : tf32_lo(h);
-          }
-          v = make_float4(x[0], x[1], x[2], x[3]);
+          for (int e = 0; e < 4; ++e) x[e] = Hh[pc_off_h<KP>(4 * jj + e, k)];
+          *reinterpret_cast<float4*>(HT + pc_off_ht(k, 4 * jj)) = make_float4(x[0], x[1], x[2], x[3]);
+          *reinterpret_cast<float4*>(HT + pc_off_ht(KP + k, 4 * jj)) =
+              make_float4(tf32_lo(x[0]), tf32_lo(x[1]), tf32_lo(x[2]), tf32_lo(x[3]));
+        } else {  // the 8 zero rows behind the lo half
+          *reinterpret_cast<float4*>(HT + pc_off_ht(KP2 + t8, 4 * jj)) = make_float4(0.f, 0.f, 0.f, 0.f);
         }
-        *reinterpret_cast<float4*>(HT + pc_off_ht(kp, n4)) = v;
       }
       proxy_fence();
       __syncthreads();
