@@ -273,6 +273,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPcThreads, 1) solve
   // exchange: bar_pfree = the peer's phase B is done (its slots take our partials), bar_xfull =
   // the peer's partials have landed in our slots (bulk copy, complete_tx)
   __shared__ __align__(8) uint64_t bar_pfree, bar_xfull;
+  __shared__ __align__(8) uint64_t bar_h;  // the peer's updated h (its frames) has landed in our Hh
   __shared__ __align__(8) uint64_t bar_hand;  // tile 0's chunks are issued (warp 0 -> warp 1)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -312,6 +313,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPcThreads, 1) solve
     mbar_init(&bar_s, 1);
     mbar_init(&bar_pfree, 1);
     mbar_init(&bar_xfull, 1);  // thread 0's arrive.expect_tx + the peer's bulk copy
+    mbar_init(&bar_h, 1);      // the same for the h block
     mbar_init(&bar_hand, 1);
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
@@ -775,8 +777,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPcThreads, 1) solve
     mbar_wait(&bar_b, pass & 1);  // (every warp is an epilogue warp)
     tc_fence_after();
     PC_MARK(8, 0);
+    // Frame ownership: rank r updates frames [32 r, 32 r + 32) only.  It needs the peer's num / den
+    // partials of those frames (half of the old exchange volume each way), and afterwards sends
+    // its block of h (hi copy, one contiguous 7 KB piece of the K-major layout) to the peer, which
+    // rebuilds the lo copy: two short DSMEM hops instead of one long one, and half the update.
+    const int own0 = 32 * int(rank), ownc = max(0, min(32, nf - own0));
+    const int peer0 = 32 * int(peer), peerc = max(0, min(32, nf - peer0));
     if (tid == 0) {
-      mbar_expect_tx(&bar_xfull, uint32_t(2 * nf * XS * sizeof(float)));  // the peer's partials, before it may send them
+      mbar_expect_tx(&bar_xfull, uint32_t(2 * ownc * XS * sizeof(float)));  // the peer's partials of our frames
+      mbar_expect_tx(&bar_h, uint32_t(4 * (KP / 4) * 32 * sizeof(float)));  // and, later, its h block
       mbar_arrive_remote(&bar_pfree, peer);  // our phase B is done: our slots may take them
     }
     {
@@ -806,38 +815,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPcThreads, 1) solve
     proxy_fence();  // the partials, for the bulk copy (async proxy)
     __syncthreads();
     PC_MARK(16, 0);
-    if (tid == 0) {  // our partials -> the same place in the peer's slots (num rows, den rows)
-      const uint32_t xrow_bytes = uint32_t(nf * XS * sizeof(float));
+    if (tid == 0) {  // our partials of the peer's frames -> the same place in the peer's slots
+      const uint32_t xrow_bytes = uint32_t(peerc * XS * sizeof(float));
       mbar_wait_cluster(&bar_pfree, pass & 1);  // the peer's phase B is done: its slots are free
       PC_MARK(9, 0);
       const uint32_t rbar = dsmem_addr(&bar_xfull, peer);
+      if (peerc > 0) {
 #pragma unroll
-      for (int nd = 0; nd < 2; ++nd) {
-        const float* src = XB + (int(rank) * 2 + nd) * kPcFrames * XS;
-        asm volatile(
-            "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                dsmem_addr(src, peer)),
-            "r"(smem_addr(src)), "r"(xrow_bytes), "r"(rbar)
-            : "memory");
+        for (int nd = 0; nd < 2; ++nd) {
+          const float* src = XB + ((int(rank) * 2 + nd) * kPcFrames + peer0) * XS;
+          asm volatile(
+              "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  dsmem_addr(src, peer)),
+              "r"(smem_addr(src)), "r"(xrow_bytes), "r"(rbar)
+              : "memory");
+        }
       }
     }
-    mbar_wait_cluster(&bar_xfull, pass & 1);  // the peer's partials have landed
+    mbar_wait_cluster(&bar_xfull, pass & 1);  // the peer's partials of our frames have landed
     PC_MARK(12, 0);
     {
-      // both CTAs: h of every frame, fixed order (own-rank-independent: rank 0 + rank 1 + tail);
-      // thread (frame n = tid % 64, k quads g, g + 4, ...) loads all its operands first.  A
-      // quarter warp touches 8 consecutive frames: conflict-free in the exchange rows (stride
-      // XS) and in the h core matrices.  Frames >= nf and atoms >= K keep h = 0.
-      constexpr int NQ = KP / 4, NI = (NQ + 3) / 4;
-      const int n = tid & 63, g = tid >> 6, nk4 = (K + 3) >> 2;
-      // two quads at a time (register budget: v + eps stays resident)
+      // our frames' h, fixed order (rank 0 + rank 1 + tail); thread (frame own0 + tid % 32, k
+      // quads g8, g8 + 8, ...) loads all its operands first.  A quarter warp touches 8 consecutive
+      // frames: conflict-free in the exchange rows (stride XS) and in the h core matrices.
+      // Frames >= nf and atoms >= K keep h = 0.
+      constexpr int NQ = KP / 4, NI = (NQ + 7) / 8;
+      const int n = own0 + (tid & 31), g8 = tid >> 5, nk4 = (K + 3) >> 2;
 #pragma unroll
       for (int i0 = 0; i0 < NI; i0 += 2) {
         if (n >= nf) break;
         float4 a0[2], a1[2], b0[2], b1[2], hq[2];
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
-          const int kq = g + 4 * (i0 + i), k4 = 4 * kq;
+          const int kq = g8 + 8 * (i0 + i), k4 = 4 * kq;
           if (i0 + i < NI && kq < nk4) {
             a0[i] = *reinterpret_cast<const float4*>(XB + (0 * kPcFrames + n) * XS + k4);
             a1[i] = *reinterpret_cast<const float4*>(XB + (2 * kPcFrames + n) * XS + k4);
@@ -849,7 +859,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPcThreads, 1) solve
         PC_MARK(34, i0);
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
-          const int kq = g + 4 * (i0 + i), k4 = 4 * kq;
+          const int kq = g8 + 8 * (i0 + i), k4 = 4 * kq;
           if (i0 + i >= NI || kq >= nk4) continue;
           float num[4] = {a0[i].x + a1[i].x, a0[i].y + a1[i].y, a0[i].z + a1[i].z, a0[i].w + a1[i].w};
           float den[4] = {b0[i].x + b1[i].x, b0[i].y + b1[i].y, b0[i].z + b1[i].z, b0[i].w + b1[i].w};
@@ -875,6 +885,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPcThreads, 1) solve
               make_float4(tf32_lo(hv[0]), tf32_lo(hv[1]), tf32_lo(hv[2]), tf32_lo(hv[3]));
         }
       }
+    }
+    PC_MARK(17, 0);
+    {
+      // our h block (hi copy) -> the peer; its block -> our Hh, lo copy rebuilt here
+      constexpr int kBlk = 4 * (KP / 4) * 32;  // floats of 32 frames of the K-major h layout
+      proxy_fence();  // the updated block, for the bulk copy (async proxy)
+      __syncthreads();
+      if (tid == 0) {
+        const float* src = Hh + int(rank) * kBlk;
+        asm volatile(
+            "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                dsmem_addr(src, peer)),
+            "r"(smem_addr(src)), "r"(uint32_t(kBlk * sizeof(float))), "r"(dsmem_addr(&bar_h, peer))
+            : "memory");
+      }
+      mbar_wait_cluster(&bar_h, pass & 1);
+      for (int i = tid; i < kBlk; i += kPcThreads) Hl[int(peer) * kBlk + i] = tf32_lo(Hh[int(peer) * kBlk + i]);
     }
     PC_MARK(17, 0);
     proxy_fence();
