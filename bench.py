@@ -345,7 +345,11 @@ def run_batch(args, rank, world):
                                        "flops_per_step": flops,
                                        "flop_model": "12FKN per epoch (H pass 6FKN + statistics 6FKN; the "
                                                      "objective shares the next epoch's first W h) + 2FKN",
-                                       "traffic": None,
+                                       "traffic": k1_traffic("c2")[0], "traffic_source": k1_traffic("c2")[1],
+                                       "traffic_unit": "bytes per K1M launch = per epoch (ncu dram__bytes_read+write)",
+                                       "algorithmic_bytes_per_launch": float(N) * (4 * F + 8 * K),
+                                       "algorithmic_bytes_note": "per epoch: V read once (4F per frame) + H read and "
+                                                                 "written in fp32 (8K per frame)",
                                        "peak_source": "mma.sync m16n8k8 tf32 1020 flop/clk/SM (tools/probe/mma_probe2.cu)"
                                                       " / 3 (3xTF32), 148 SM x 1.965 GHz",
                                        "fp32_roofline": {"peak": peak, "frac": flops / t / 1e12 / peak,
