@@ -830,6 +830,7 @@ int launch_block(isnmf_online* c, const float* dv, int64_t ldv, int nb, const ui
   FoldArgs r = fold_args(c);
   r.nstat = chained ? (nblk + c->plan.chain - 1) / c->plan.chain : nblk;
   r.stats_tiled = chained ? 1 : c->plan.tiled ? 2 : 0;
+  r.after_k1 = 1;
   r.ndiv = (c->plan.pair || c->plan.mpair) ? 2 * nblk : nblk;
   r.nframes = nb;
   r.do_commit = commit;

@@ -1040,6 +1040,7 @@ struct FoldArgs {
   double* scale_out;  // optional: column scales s_k of this commit (batch H compensation)
   int batch_mode;
   int stats_cap;      // planes / divergence partials allocated (debug checks; 0 = unchecked)
+  int after_k1;       // this launch follows a K1 launch (the previous commit completed before that K1 started)
   int stats_tiled;    // 1: K1T's chained layout [window of 32 rows][sa|sb][KP][32], rows swizzled by k; 2: K1M's
                       // [window of 16 rows][sa|sb][K][16] (kernels_mma.cuh mm_plane_off)
   long long p_cap;    // rows of P (debug checks; 0 = unchecked)
@@ -1164,6 +1165,15 @@ __global__ void __cluster_dims__(kFoldCluster, 1, 1) __launch_bounds__(kFoldThre
     }
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
+  // the commit count and the column's prefix product (the P row of this commit's predecessor)
+  // for the warm-store table: two dependent L2 loads, taken off the rescale phase
+  unsigned long long c_prev = 0;
+  double p_prev = 1.0;
+  const bool early_p = a.after_k1 != 0;  // (a K2 that directly follows another may still see the old count)
+  if (early_p && a.do_commit && !a.batch_mode && r == 0 && tid == 0) {
+    c_prev = a.st->commits;
+    p_prev = a.P[size_t(c_prev) * a.K + k];
+  }
   // the row state above is written only by the previous K2 (complete before the K1 that
   // precedes this grid started); the partials and the status come from that K1
   pdl_wait();
@@ -1322,8 +1332,11 @@ __global__ void __cluster_dims__(kFoldCluster, 1, 1) __launch_bounds__(kFoldThre
     }
   }
   if (ok && r == 0 && tid == 0) {
-    const unsigned long long c = a.st->commits;
-    if (!a.batch_mode) a.P[size_t(c + 1) * a.K + k] = a.P[size_t(c) * a.K + k] * sc;
+    if (!a.batch_mode && !early_p) {
+      c_prev = a.st->commits;
+      p_prev = a.P[size_t(c_prev) * a.K + k];
+    }
+    if (!a.batch_mode) a.P[size_t(c_prev + 1) * a.K + k] = p_prev * sc;
     if (a.scale_out) a.scale_out[k] = sc;
   }
   if (!ok && tid == 0) atomicOr(&a.st->pad, ST_ZERO_COLUMN);
