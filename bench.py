@@ -315,11 +315,14 @@ def run_batch(args, rank, world):
         vh.copy_(vd)
         E.batch_train(vh, w0, h0, 1)
         t0 = time.perf_counter()
+        calls = []
         for _ in range(args.steps):
+            tc = time.perf_counter()
             E.batch_train(vh, w0, h0, epochs)
+            calls.append(round(1e3 * (time.perf_counter() - tc), 1))
         e2e_s = allmax((time.perf_counter() - t0) / args.steps, world)
-        e2e = {"value": world * epochs / e2e_s, "unit": "epochs/s", "h2d_bytes_per_step": int(N * F * 4 + K * N * 4),
-               "d2h_bytes_per_step": int(K * N * 4 + F * K * 8),
+        e2e = {"value": world * epochs / e2e_s, "unit": "epochs/s", "h2d_bytes_per_step": int(N * F * 4 + K * N * 8),
+               "d2h_bytes_per_step": int(K * N * 8 + F * K * 8), "calls_ms": calls,
                "timing": "host wall clock of the whole batch_train call with V in pinned host memory"}
     cpu = None
     if rank == 0 and not args.no_cpu:
