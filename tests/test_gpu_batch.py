@@ -86,3 +86,14 @@ def test_batch_errors():
     with pytest.raises(E.EngineError) as e:
         E.batch_train(v, np.zeros((5, 2)), np.ones((2, 4)), 3)
     assert e.value.kind == "NonPositiveInit"
+    h0 = np.ones((2, 4))
+    h0[1, 2] = 0.0  # checked on the device while H0 is converted
+    with pytest.raises(E.EngineError) as e:
+        E.batch_train(v, np.ones((5, 2)), h0, 3)
+    assert e.value.kind == "NonPositiveInit"
+    h0[1, 2] = np.nan
+    with pytest.raises(E.EngineError) as e:
+        E.batch_train(v, np.ones((5, 2)), h0, 3)
+    assert e.value.kind == "NonPositiveInit"
+    out = E.batch_train(v, np.ones((5, 2)), np.ones((2, 4)), 3)  # the context is usable afterwards
+    assert out["epochs"] == 3
