@@ -210,6 +210,39 @@ def cpu_baseline(cfg, v_host_cols, w0, a0, threads, batches):
     return n / dt, dt, n
 
 
+def reference_build_rate(cfg, v_host_cols, w0, a0, frames):
+    """The reference's OWN online trainer (online_resume / online_step / dictionary_commit, headers
+    compiled unchanged over the test-only Eigen-subset shim: oracle/_ref/ref_trainer, built by
+    `make -C oracle ref` where /root/reference exists) on `frames` frames of this shape, 1 core.
+    Returns (frames/s, seconds) from the trainer's own loop, or None when the binary is absent."""
+    import struct
+    import subprocess
+    import tempfile
+    exe = os.path.join(ROOT, "oracle", "_ref", "ref_trainer")
+    if not os.access(exe, os.X_OK):
+        return None
+
+    def write_isnm(path, m):
+        m = np.asfortranarray(m, dtype=np.float64)
+        with open(path, "wb") as f:
+            f.write(b"ISNM" + struct.pack("<IQQ", 1, m.shape[0], m.shape[1]))
+            f.write(m.tobytes(order="F"))
+    try:
+        with tempfile.TemporaryDirectory() as d:
+            write_isnm(os.path.join(d, "v.isnm"), v_host_cols[:, :frames])
+            write_isnm(os.path.join(d, "w0.isnm"), w0)
+            with open(os.path.join(d, "params.txt"), "w") as f:
+                f.write(f"beta {cfg['beta']}\niters {cfg['iters']}\nrho {cfg['rho']!r}\nrestart warm\nseed 1\n"
+                        f"eps 1e-12\nbudget {frames}\na0 {float(a0.flat[0])!r}\nh0 1.0\norder in_order\n")
+            subprocess.run([exe, "online", d], check=True, timeout=600, stdout=subprocess.DEVNULL,
+                           stderr=subprocess.DEVNULL)
+            st = dict(line.split() for line in open(os.path.join(d, "state.txt")))
+            sec = float(st["train_seconds"])
+            return frames / sec, sec
+    except Exception:  # noqa: BLE001 (a reported extra, never fatal to the bench)
+        return None
+
+
 def host_info():
     cpu = "unknown"
     try:
@@ -556,7 +589,15 @@ def run_engine(args, rank, world):
         cpu = {"value": r, "unit": "frames/s", "cores": 1, "kind": "port",
                "sample": f"first {batches} mini-batches ({n} frames, {dt:.1f} s) of the {args.config} shape, "
                          f"fp64 oracle restatement of the reference path on 1 core of {cpu_name} "
-                         f"({ncpu} cores); the reference itself cannot be compiled (no Eigen)"}
+                         f"({ncpu} cores); the reference needs Eigen, which is not installed"}
+        nref = beta * min(2, batches)
+        rb = reference_build_rate(cfg, vs, w0, a0, nref)
+        if rb:
+            cpu["reference_build"] = {
+                "value": rb[0], "unit": "frames/s", "cores": 1, "kind": "reference",
+                "sample": f"{nref} frames ({rb[1]:.1f} s in the trainer's own loop): the reference's online_resume "
+                          "compiled unchanged over the test-only Eigen-subset shim (oracle/ref), 1 core; the shim "
+                          "evaluates eagerly, so real Eigen would be faster - the port above is the stronger baseline"}
 
     traffic, traffic_src = k1_traffic(args.config)
     compare = None

@@ -24,6 +24,7 @@
 //           commit), state.txt (t commits last_minibatch_obj last_delta
 //           pending_count pending_div rho)
 //   batch:  w.isnm h.isnm, trace.txt (epoch obj delta)
+#include <chrono>
 #include <cstdio>
 #include <fstream>
 #include <map>
@@ -145,7 +146,9 @@ int run_online(const std::string& dir) {
     }
     return true;
   };
+  const auto t0 = std::chrono::steady_clock::now();
   online_resume(st, src, cfg, cb, [] { return 0.0; });
+  const double train_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   tr.close();
   save_matrix(dir + "/w.isnm", st.dict.w);
   save_matrix(dir + "/a.isnm", st.dict.a);
@@ -157,7 +160,7 @@ int run_online(const std::string& dir) {
   so.precision(17);
   so << "t " << st.t << "\ncommits " << st.commits << "\nlast_minibatch_obj " << st.last_minibatch_obj
      << "\nlast_delta " << st.last_delta << "\npending_count " << st.pending_count << "\npending_div "
-     << st.pending_div << "\nrho " << st.rho << "\n";
+     << st.pending_div << "\nrho " << st.rho << "\ntrain_seconds " << train_seconds << "\n";
   return 0;
 }
 
