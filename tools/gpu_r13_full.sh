@@ -1,7 +1,7 @@
 #!/bin/bash
 # Round-2 (session 6, after the K1C h^T / frame-ownership, K2 and prefetch changes) evidence: -m gpu suite, smoke, driver c3 bench, reference arm, other configs,
-# launch list and ncu --set full of the c3 solve kernel (K1C).  Output under gpurun_out/r12/.
-O=gpurun_out/r12; mkdir -p $O
+# launch list and ncu --set full of the c3 solve kernel (K1C).  Output under gpurun_out/r13/.
+O=gpurun_out/r13; mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > $O/smi.txt 2>&1
 timeout 1500 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" | tee -a $O/pytest_gpu.log; tail -3 $O/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?"; tail -1 $O/smoke.log
