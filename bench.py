@@ -493,10 +493,13 @@ def run_engine(args, rank, world):
 
     eng = E.Online(F, K, beta, iters, restart="warm", n_store=N)
 
+    zero_fk = np.zeros((F, K), order="F")
+
     def reinit():
-        """Config 3's initial state (W0, A0 = B0 = 1e-3, t = commits = 0, warm store
-        h0 = 1): every step is exactly one config-3 pass, not a continuation."""
+        """Config 3's initial state (W0, A0 = B0 = 1e-3, no pending statistics, t = commits = 0,
+        warm store h0 = 1): every step is exactly one config-3 pass, not a continuation."""
         eng.set_dictionary(w0, a0, a0)
+        eng.set_pending(zero_fk, zero_fk, 0.0, 0)  # (the N mod beta leftover frames of the previous pass)
         eng.set_counters(0, 0, rho)
         eng.fill_warm_h(1.0)
 
